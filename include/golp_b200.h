@@ -1,0 +1,143 @@
+/*
+ * golp_b200.h -- C ABI of libgolp_b200.so, the B200 offload path for the
+ * reference `golp` package (arXiv 2601.19911, /root/reference/pkg/src/golp).
+ *
+ * The reference's plug-in boundary is the duck-typed device protocol
+ * {name, topk(), probe(), close()} that gate._run_query calls
+ * (pkg/src/golp/gate.py:185-213) and make_device() constructs
+ * (pkg/src/golp/device.py:439-445). Each entry point below replaces one step of
+ * that protocol; see INTEGRATION.md for the ctypes binding a golp maintainer adds.
+ *
+ * Conventions
+ *   - plain pointers and sizes; no torch / CUDA types in signatures
+ *     (streams are passed as an opaque `void*` = cudaStream_t, NULL = default);
+ *   - every function returns a golp_status; golp_last_error() describes the
+ *     last failure of the calling process;
+ *   - calls are externally synchronous, one call at a time per process, exactly
+ *     like the reference's ProxyDevice ("one call, one ledger");
+ *   - the library never writes to input buffers and never retains input
+ *     pointers after a call returns.
+ */
+#ifndef GOLP_B200_H
+#define GOLP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum golp_status {
+  GOLP_OK = 0,
+  GOLP_ERR_INVALID = 1,  /* -> ValueError (device.py:336-337, device.py:144-151) */
+  GOLP_ERR_CAPACITY = 2, /* -> CapacityError (host.py:155-159)                  */
+  GOLP_ERR_CUDA = 3      /* -> RuntimeError                                     */
+} golp_status;
+
+typedef enum golp_mode {
+  GOLP_KEY_ONLY = 0, /* 12 B per entry: f64 key + u32 row id (store.py:23-26) */
+  GOLP_FULL_ROW = 1  /* 8 + payload_bytes per row (device.py:144-151)         */
+} golp_mode;
+
+/* Mirrors TransferLedger (pkg/src/golp/device.py:98-126). Byte counts follow
+ * the reference's shape formulas (device.py:372-379, 428-435), never measured;
+ * phase times are seconds on the critical path, so their sum is the wall time
+ * of the call. */
+typedef struct golp_ledger {
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
+  double t_h2d;
+  double t_kernel;
+  double t_d2h;
+  double t_post;
+} golp_ledger;
+
+/* Device-time breakdown of the last call (CUDA events on the launching stream;
+ * filled only while golp_set_profiling(1) is active). Milliseconds. */
+typedef struct golp_kernel_times {
+  double topk_threshold_ms;
+  double topk_filter_ms;
+  double topk_select_ms;
+  double join_build_ms;
+  double join_probe_ms;
+  uint64_t topk_candidates; /* survivors of the streaming filter          */
+  uint64_t topk_fallback;   /* 1 if the exact direct path had to run       */
+  uint64_t join_groups;     /* distinct build keys                         */
+  uint64_t join_capacity;   /* hash-table slots                            */
+} golp_kernel_times;
+
+/* ---- lifecycle ---------------------------------------------------------------- */
+const char* golp_last_error(void);
+int golp_version(void);
+/* Select the CUDA device and size the pinned staging ring (0 = defaults).
+ * Replaces ProxyDevice.__init__ (device.py:308-310). Implicit on first use. */
+int golp_init(int device, uint64_t pinned_chunk_bytes, int host_threads);
+/* Frees device buffers, pinned staging and streams. Replaces
+ * ProxyDevice.close (device.py:312-315). */
+int golp_shutdown(void);
+/* Number of CUDA kernels this library has launched (process lifetime). */
+uint64_t golp_launch_count(void);
+int golp_set_profiling(int on);
+int golp_last_kernel_times(golp_kernel_times* out);
+
+/* ---- host-buffer entry points: ProxyDevice.topk / ProxyDevice.probe ------------ */
+/* Replaces ProxyDevice.topk (pkg/src/golp/device.py:329-380). keys/rows are the
+ * KeyVector columns (store.py:75-112). Writes min(k, n) row ids, best first:
+ * keys descending, equal keys by ascending row id (host.py:133-144).
+ * k < 1 -> GOLP_ERR_INVALID. FULL_ROW additionally ships n*payload_bytes bytes. */
+int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, int mode,
+              uint32_t payload_bytes, uint32_t* out_rows, uint64_t* out_len, golp_ledger* led);
+
+/* Replaces ProxyDevice.probe (pkg/src/golp/device.py:382-436), phase 1 of 2:
+ * ships both sides, builds, probes, and reports the match count M. The pairs
+ * stay in library-owned device memory until golp_probe_copy_out. */
+int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb,
+               const double* probe_keys, const uint32_t* probe_rows, uint64_t np, int mode,
+               uint32_t payload_bytes, uint64_t* out_matches, golp_ledger* led);
+/* Phase 2: copy the M pairs of the last golp_probe into caller arrays (each of
+ * m = M entries), in reference order: probe position, then build insertion
+ * position (host.py:168-188). Adds t_d2h and d2h_bytes = 8*M to *led. */
+int golp_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m, golp_ledger* led);
+
+/* ---- device-resident entry points (inputs already in HBM) ---------------------- */
+/* Top-K of n device-resident items. d_out_rows gets min(k, n) rows best first;
+ * d_out_keys (optional, may be NULL) gets their order-preserving u64 key codes
+ * (for cross-GPU merges via golp_topk_merge_device). */
+int golp_topk_device(const double* d_keys, const uint32_t* d_rows, uint64_t n, uint64_t k,
+                     uint32_t* d_out_rows, uint64_t* d_out_keys, void* stream);
+/* Exact Top-K of n already-encoded candidates (u64 key code, u32 row), e.g. the
+ * all-gathered local results of G GPUs. Same output contract as above. */
+int golp_topk_merge_device(const uint64_t* d_key_codes, const uint32_t* d_rows, uint64_t n, uint64_t k,
+                           uint32_t* d_out_rows, uint64_t* d_out_keys, void* stream);
+/* Build the library's join table from nb device-resident build entries
+ * (host_hash_build, host.py:147-165; insertion order = position order). */
+int golp_join_build_device(const double* d_build_keys, const uint32_t* d_build_rows, uint64_t nb,
+                           void* stream);
+/* Probe the table built last. Writes min(M, cap) pairs and sets *out_matches = M;
+ * returns GOLP_ERR_CAPACITY (pairs truncated) when M > cap. */
+int golp_join_probe_device(const double* d_probe_keys, const uint32_t* d_probe_rows, uint64_t np,
+                           uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
+                           uint64_t* out_matches, void* stream);
+
+/* ---- classical host engine (the gate's HOST path, gate.py:193-194,209-210) ------ */
+/* Multi-threaded CPU Top-K with host_topk's exact output (host.py:133-144). */
+int golp_host_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, uint32_t* out_rows,
+                   int threads);
+/* KeyHashTable build with the reference's slot layout (host.py:83-165):
+ * capacity = smallest power of two >= 8 with capacity*0.7 >= n; serial
+ * insertion in position order; linear probing on mix64(key_bits). The caller
+ * passes zeroed slot_bits and ROW_EMPTY-filled slot_rows of `capacity` entries. */
+int golp_host_hash_build(const double* keys, const uint32_t* rows, uint64_t n, uint64_t capacity,
+                         uint64_t* slot_bits, uint32_t* slot_rows);
+/* host_hash_probe (host.py:168-188) on such a table, chunk-parallel over the
+ * probe side. Phase 1 of 2: sets *out_matches = M and keeps the pairs. */
+int golp_host_hash_probe(const uint64_t* slot_bits, const uint32_t* slot_rows, uint64_t capacity,
+                         const double* keys, const uint32_t* rows, uint64_t n, int threads,
+                         uint64_t* out_matches);
+/* Phase 2: copy the M pairs of the last golp_host_hash_probe, reference order. */
+int golp_host_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GOLP_B200_H */

@@ -1,0 +1,131 @@
+"""ctypes binding of libgolp_b200.so (C ABI in include/golp_b200.h).
+
+The library is the product: there is no Python or CPU fallback for the device
+path. If the shared object is missing or fails to load, every device entry
+point raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+from .errors import CapacityError
+
+LIB_PATH = Path(__file__).resolve().parent / "libgolp_b200.so"
+
+GOLP_OK = 0
+GOLP_ERR_INVALID = 1
+GOLP_ERR_CAPACITY = 2
+GOLP_ERR_CUDA = 3
+
+GOLP_KEY_ONLY = 0
+GOLP_FULL_ROW = 1
+
+_vp = C.c_void_p
+_u64 = C.c_uint64
+_u32 = C.c_uint32
+_int = C.c_int
+
+
+class Ledger(C.Structure):
+    _fields_ = [
+        ("h2d_bytes", C.c_uint64),
+        ("d2h_bytes", C.c_uint64),
+        ("t_h2d", C.c_double),
+        ("t_kernel", C.c_double),
+        ("t_d2h", C.c_double),
+        ("t_post", C.c_double),
+    ]
+
+
+class KernelTimes(C.Structure):
+    _fields_ = [
+        ("topk_threshold_ms", C.c_double),
+        ("topk_filter_ms", C.c_double),
+        ("topk_select_ms", C.c_double),
+        ("join_build_ms", C.c_double),
+        ("join_probe_ms", C.c_double),
+        ("topk_candidates", C.c_uint64),
+        ("topk_fallback", C.c_uint64),
+        ("join_groups", C.c_uint64),
+        ("join_capacity", C.c_uint64),
+    ]
+
+
+# name -> (restype, argtypes); mirrors include/golp_b200.h one to one
+SIGNATURES = {
+    "golp_last_error": (C.c_char_p, []),
+    "golp_version": (_int, []),
+    "golp_init": (_int, [_int, _u64, _int]),
+    "golp_shutdown": (_int, []),
+    "golp_launch_count": (_u64, []),
+    "golp_set_profiling": (_int, [_int]),
+    "golp_last_kernel_times": (_int, [C.POINTER(KernelTimes)]),
+    "golp_topk": (_int, [_vp, _vp, _u64, _u64, _int, _u32, _vp, C.POINTER(_u64), C.POINTER(Ledger)]),
+    "golp_probe": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, _int, _u32, C.POINTER(_u64), C.POINTER(Ledger)]),
+    "golp_probe_copy_out": (_int, [_vp, _vp, _u64, C.POINTER(Ledger)]),
+    "golp_topk_device": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
+    "golp_topk_merge_device": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
+    "golp_join_build_device": (_int, [_vp, _vp, _u64, _vp]),
+    "golp_join_probe_device": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, C.POINTER(_u64), _vp]),
+    "golp_host_topk": (_int, [_vp, _vp, _u64, _u64, _vp, _int]),
+    "golp_host_hash_build": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),
+    "golp_host_hash_probe": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, _int, C.POINTER(_u64)]),
+    "golp_host_probe_copy_out": (_int, [_vp, _vp, _u64]),
+}
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load (once) and type the shared library; raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("GOLP_B200_LIB", LIB_PATH))
+    if not path.exists():
+        raise RuntimeError(
+            f"{path} is not built: the B200 path has no fallback. "
+            "Run `python -c 'import __graft_entry__ as g; g.build()'` first."
+        )
+    lib = C.CDLL(str(path))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    msg = load().golp_last_error()
+    return msg.decode("utf-8", "replace") if msg else ""
+
+
+def check(rc: int) -> None:
+    """Map a golp_status onto the reference's exception types (errors.py)."""
+    if rc == GOLP_OK:
+        return
+    msg = last_error()
+    if rc == GOLP_ERR_INVALID:
+        raise ValueError(msg)
+    if rc == GOLP_ERR_CAPACITY:
+        raise CapacityError(msg)
+    raise RuntimeError(f"libgolp_b200: {msg}")
+
+
+def ptr(arr) -> int:
+    """Address of a numpy array's first element (0 for empty arrays)."""
+    return int(arr.ctypes.data) if arr.size else 0
+
+
+def launch_count() -> int:
+    return int(load().golp_launch_count())
+
+
+def kernel_times() -> dict:
+    kt = KernelTimes()
+    check(load().golp_last_kernel_times(C.byref(kt)))
+    return {name: getattr(kt, name) for name, _ in KernelTimes._fields_}

@@ -1,0 +1,849 @@
+// C ABI of libgolp_b200.so (declared in include/golp_b200.h): device context,
+// HBM workspace, pinned staging ring, stream/event orchestration and ledgers.
+//
+// Boundary being replaced: the reference's device protocol topk()/probe()
+// (ProxyDevice, pkg/src/golp/device.py:299-436), whose ledgers feed the gate
+// (pkg/src/golp/gate.py:185-213) and calibrate_profile (device.py:490-554).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "../../include/golp_b200.h"
+#include "join.cuh"
+#include "runtime.h"
+#include "topk.cuh"
+
+namespace golp {
+const char* last_error_cstr();
+}
+
+using namespace golp;
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) {                                                               \
+      set_error(std::string(#x) + " failed: " + cudaGetErrorString(e_));                   \
+      return GOLP_ERR_CUDA;                                                                \
+    }                                                                                      \
+  } while (0)
+#define CKL() CK(cudaGetLastError())
+#define RET(x)                   \
+  do {                           \
+    int r_ = (x);                \
+    if (r_ != GOLP_OK) return r_; \
+  } while (0)
+
+int invalid(const std::string& msg) {
+  set_error(msg);
+  return GOLP_ERR_INVALID;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    const size_t alloc = std::max<size_t>(want + want / 8, 256);
+    cudaError_t e = cudaMalloc(&p, alloc);
+    if (e == cudaSuccess) bytes = alloc;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+constexpr int kSlots = 4;
+constexpr int kNumCtl = 3;  // 0: threshold select, 1: candidate select (+filter count), 2: fallback
+
+struct Ctx {
+  bool ready = false;
+  int device = 0;
+  int sms = 148;
+  cudaStream_t s_main = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+  size_t chunk = 32u << 20;
+  void* pin[kSlots] = {};
+  cudaEvent_t pin_ev[kSlots] = {};
+  bool pin_busy[kSlots] = {};
+  int next_slot = 0;
+  void* pin_small = nullptr;  // samples, counters, small outputs
+  size_t pin_small_bytes = 16u << 20;
+  WorkerPool pool;
+  cudaEvent_t ev[8] = {};
+
+  DevBuf ctl, cand_hi, cand_lo, w_hi, w_lo, out_rows, out_hi, samples;
+  DevBuf table, bslot, brank, csr_pos, csr_row, big_list, jcount, tile_status, tile_counter, totals;
+  DevBuf pairs_p, pairs_b;
+  DevBuf in_keys, in_rows, in_bkeys, in_brows, in_payload;
+  uint64_t jcap = 0, jmask = 0, jnb = 0;
+  uint64_t last_m = 0;
+  bool last_probe_valid = false;
+
+  bool prof = false;
+  golp_kernel_times kt{};
+};
+
+Ctx g;
+
+int do_init(int device, uint64_t chunk_bytes, int host_threads) {
+  if (g.ready) return GOLP_OK;
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (ndev <= 0) {
+    set_error("no CUDA device visible");
+    return GOLP_ERR_CUDA;
+  }
+  if (device < 0) CK(cudaGetDevice(&device));
+  CK(cudaSetDevice(device));
+  g.device = device;
+  CK(cudaDeviceGetAttribute(&g.sms, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaStreamCreateWithFlags(&g.s_main, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&g.s_h2d, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&g.s_d2h, cudaStreamNonBlocking));
+  if (chunk_bytes) g.chunk = (size_t)chunk_bytes;
+  for (int i = 0; i < kSlots; ++i) {
+    CK(cudaHostAlloc(&g.pin[i], g.chunk, cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&g.pin_ev[i], cudaEventDisableTiming));
+    g.pin_busy[i] = false;
+  }
+  CK(cudaHostAlloc(&g.pin_small, g.pin_small_bytes, cudaHostAllocDefault));
+  for (auto& e : g.ev) CK(cudaEventCreate(&e));
+  int hw = (int)std::thread::hardware_concurrency();
+  if (host_threads <= 0) host_threads = std::max(1, std::min(8, hw - 1));
+  g.pool.start(host_threads);
+  CK(g.ctl.ensure(sizeof(SelectCtl) * kNumCtl));
+  g.ready = true;
+  return GOLP_OK;
+}
+
+int ensure_init() { return g.ready ? GOLP_OK : do_init(-1, 0, 0); }
+
+SelectCtl* ctl(int i) { return g.ctl.as<SelectCtl>() + i; }
+
+// ---- pinned staging ring ----------------------------------------------------------
+// Host -> device copy of an arbitrary pageable buffer: the pool packs chunk i+1
+// into a pinned slot while the DMA engine drains chunk i.
+int stage_h2d(void* dst, const void* src, size_t bytes) {
+  size_t done = 0;
+  while (done < bytes) {
+    const int slot = g.next_slot;
+    g.next_slot = (g.next_slot + 1) % kSlots;
+    if (g.pin_busy[slot]) CK(cudaEventSynchronize(g.pin_ev[slot]));
+    const size_t len = std::min(g.chunk, bytes - done);
+    parallel_copy(g.pool, g.pin[slot], static_cast<const char*>(src) + done, len);
+    CK(cudaMemcpyAsync(static_cast<char*>(dst) + done, g.pin[slot], len, cudaMemcpyHostToDevice, g.s_h2d));
+    CK(cudaEventRecord(g.pin_ev[slot], g.s_h2d));
+    g.pin_busy[slot] = true;
+    done += len;
+  }
+  return GOLP_OK;
+}
+
+// Full-row mode ships payload bytes the device never reads: stream a pinned slot
+// (contents irrelevant) into a device scratch chunk, repeatedly.
+int stage_dummy_h2d(size_t bytes) {
+  if (!bytes) return GOLP_OK;
+  CK(g.in_payload.ensure(g.chunk));
+  size_t done = 0;
+  while (done < bytes) {
+    const int slot = g.next_slot;
+    g.next_slot = (g.next_slot + 1) % kSlots;
+    if (g.pin_busy[slot]) CK(cudaEventSynchronize(g.pin_ev[slot]));
+    const size_t len = std::min(g.chunk, bytes - done);
+    CK(cudaMemcpyAsync(g.in_payload.p, g.pin[slot], len, cudaMemcpyHostToDevice, g.s_h2d));
+    CK(cudaEventRecord(g.pin_ev[slot], g.s_h2d));
+    g.pin_busy[slot] = true;
+    done += len;
+  }
+  return GOLP_OK;
+}
+
+// Device -> host copy into pageable memory through the same ring.
+int stage_d2h(void* dst, const void* src, size_t bytes) {
+  size_t done = 0;
+  int inflight_slot[kSlots] = {};
+  size_t inflight_off[kSlots] = {}, inflight_len[kSlots] = {};
+  int q = 0;
+  auto drain_one = [&](int idx) -> int {
+    CK(cudaEventSynchronize(g.pin_ev[inflight_slot[idx]]));
+    parallel_copy(g.pool, static_cast<char*>(dst) + inflight_off[idx], g.pin[inflight_slot[idx]],
+                  inflight_len[idx]);
+    g.pin_busy[inflight_slot[idx]] = false;
+    return GOLP_OK;
+  };
+  // simple in-order pipeline: keep up to kSlots-1 copies in flight
+  int head = 0;
+  while (done < bytes) {
+    if (q - head >= kSlots - 1) {
+      RET(drain_one(head % kSlots));
+      ++head;
+    }
+    const int slot = g.next_slot;
+    g.next_slot = (g.next_slot + 1) % kSlots;
+    if (g.pin_busy[slot]) CK(cudaEventSynchronize(g.pin_ev[slot]));
+    const size_t len = std::min(g.chunk, bytes - done);
+    CK(cudaMemcpyAsync(g.pin[slot], static_cast<const char*>(src) + done, len, cudaMemcpyDeviceToHost, g.s_d2h));
+    CK(cudaEventRecord(g.pin_ev[slot], g.s_d2h));
+    g.pin_busy[slot] = true;
+    inflight_slot[q % kSlots] = slot;
+    inflight_off[q % kSlots] = done;
+    inflight_len[q % kSlots] = len;
+    ++q;
+    done += len;
+  }
+  while (head < q) {
+    RET(drain_one(head % kSlots));
+    ++head;
+  }
+  return GOLP_OK;
+}
+
+int sync_ring() {
+  for (int i = 0; i < kSlots; ++i) {
+    if (g.pin_busy[i]) CK(cudaEventSynchronize(g.pin_ev[i]));
+    g.pin_busy[i] = false;
+  }
+  return GOLP_OK;
+}
+
+// ---- Top-K planning ---------------------------------------------------------------
+struct TopkPlan {
+  bool direct;      // select straight over the input (no sampled threshold)
+  uint64_t s;       // samples
+  uint64_t need_s;  // rank of the threshold sample (1-based)
+  uint64_t cap;     // candidate capacity
+};
+
+// With S stratified samples and K' = min(k, n), the number X of samples that
+// fall in the true top K' is ~Binomial(S, K'/n). Taking the threshold at sample
+// rank r = lam + 6 sqrt(lam) + 7 (lam = S K'/n) makes P(X >= r), the only way the
+// filter can keep fewer than K' items, negligible; expected survivors ~ r n / S.
+TopkPlan plan_topk(uint64_t n, uint64_t kk) {
+  TopkPlan p{true, 0, 0, 0};
+  if (n <= kSortTile) return p;
+  uint64_t s = n / 256;
+  s = std::max<uint64_t>(2048, std::min<uint64_t>(s, 262144));
+  const double lam = (double)s * (double)kk / (double)n;
+  const uint64_t need_s = (uint64_t)std::ceil(lam + 6.0 * std::sqrt(lam) + 7.0);
+  if (need_s * 4 >= s) return p;
+  const uint64_t expect = (uint64_t)std::ceil((double)need_s * (double)n / (double)s);
+  p.direct = false;
+  p.s = s;
+  p.need_s = need_s;
+  p.cap = std::min<uint64_t>(n, std::max<uint64_t>(4 * expect + 65536, 1u << 20));
+  return p;
+}
+
+template <class Src>
+int launch_select(const SelectArgs<Src>& a, cudaStream_t s) {
+  static int blocks = 0;
+  const size_t smem = (size_t)kSortTile * (sizeof(uint64_t) + sizeof(uint32_t));
+  if (!blocks) {
+    CK(cudaFuncSetAttribute(select_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, select_kernel<Src>, kSelThreads, smem));
+    if (per < 1) {
+      set_error("select_kernel cannot be co-resident");
+      return GOLP_ERR_CUDA;
+    }
+    blocks = per * g.sms;
+  }
+  void* args[] = {const_cast<SelectArgs<Src>*>(&a)};
+  CK(cudaLaunchCooperativeKernel((const void*)select_kernel<Src>, dim3(blocks), dim3(kSelThreads), args, smem, s));
+  ++g_launches;
+  return GOLP_OK;
+}
+
+template <class Src>
+SelectArgs<Src> make_args(Src src, uint64_t n, uint64_t need, int mode, int c, uint32_t* out_rows,
+                          uint64_t* out_hi) {
+  SelectArgs<Src> a;
+  a.src = src;
+  a.n = n;
+  a.need = need;
+  a.cap = 0;
+  a.use_cand_count = 0;
+  a.mode = mode;
+  a.ctl = ctl(c);
+  a.w_hi = g.w_hi.as<uint64_t>();
+  a.w_lo = g.w_lo.as<uint32_t>();
+  a.out_rows = out_rows;
+  a.out_hi = out_hi;
+  return a;
+}
+
+int ensure_topk_ws(uint64_t kk, uint64_t cap) {
+  CK(g.w_hi.ensure(std::max<uint64_t>(kk, 1) * 8));
+  CK(g.w_lo.ensure(std::max<uint64_t>(kk, 1) * 4));
+  if (cap) {
+    CK(g.cand_hi.ensure(cap * 8));
+    CK(g.cand_lo.ensure(cap * 4));
+  }
+  return GOLP_OK;
+}
+
+int launch_filter(const double* keys, const uint32_t* rows, uint64_t n, uint64_t cap, cudaStream_t s) {
+  if (n == 0) return GOLP_OK;
+  const uint64_t vec = n / 2 + 1;
+  uint64_t blocks = (vec + (uint64_t)kFilterThreads * kFilterUnroll - 1) / ((uint64_t)kFilterThreads * kFilterUnroll);
+  blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)g.sms * 8));
+  topk_filter_kernel<<<(unsigned)blocks, kFilterThreads, 0, s>>>(keys, rows, n, ctl(0), &ctl(1)->cand_count,
+                                                                  g.cand_hi.as<uint64_t>(), g.cand_lo.as<uint32_t>(),
+                                                                  cap);
+  CKL();
+  ++g_launches;
+  return GOLP_OK;
+}
+
+void prof_record(int idx, cudaStream_t s) {
+  if (g.prof) cudaEventRecord(g.ev[idx], s);
+}
+double prof_ms(int a, int b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, g.ev[a], g.ev[b]) != cudaSuccess) return 0.0;
+  return (double)ms;
+}
+
+// Reads ctl(1) status / candidate count after a sampled run (synchronises s).
+int read_topk_status(cudaStream_t s, int* bad, uint64_t* cands) {
+  struct Tail {
+    unsigned long long cand_count;
+    int status;
+  };
+  Tail* t = static_cast<Tail*>(g.pin_small);
+  CK(cudaMemcpyAsync(&t->cand_count, &ctl(1)->cand_count, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&t->status, &ctl(1)->status, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *bad = t->status != 0;
+  *cands = t->cand_count;
+  return GOLP_OK;
+}
+
+// Exact fallback: radix select straight over the device-resident input.
+int topk_direct(const double* keys, const uint32_t* rows, uint64_t n, uint64_t kk, uint32_t* out_rows,
+                uint64_t* out_hi, cudaStream_t s) {
+  CK(cudaMemsetAsync(ctl(2), 0, sizeof(SelectCtl), s));
+  RET(launch_select(make_args(SrcInput{keys, rows}, n, kk, kModeFull, 2, out_rows, out_hi), s));
+  return GOLP_OK;
+}
+
+// Top-K over device-resident columns (sampling on the device).
+int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, uint32_t* out_rows,
+                     uint64_t* out_hi, cudaStream_t s) {
+  const uint64_t kk = std::min(k, n);
+  if (kk == 0) return GOLP_OK;
+  const TopkPlan p = plan_topk(n, kk);
+  RET(ensure_topk_ws(kk, p.direct ? 0 : p.cap));
+  g.kt.topk_fallback = 0;
+  g.kt.topk_candidates = 0;
+  prof_record(0, s);
+  if (p.direct) {
+    RET(topk_direct(keys, rows, n, kk, out_rows, out_hi, s));
+    prof_record(1, s);
+    prof_record(2, s);
+    prof_record(3, s);
+    CK(cudaStreamSynchronize(s));
+  } else {
+    CK(cudaMemsetAsync(ctl(0), 0, sizeof(SelectCtl) * 2, s));
+    RET(launch_select(make_args(SrcSample{keys, rows, n, p.s}, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), s));
+    prof_record(1, s);
+    RET(launch_filter(keys, rows, n, p.cap, s));
+    prof_record(2, s);
+    SelectArgs<SrcCand> a = make_args(SrcCand{g.cand_hi.as<uint64_t>(), g.cand_lo.as<uint32_t>()}, 0, kk,
+                                      kModeFull, 1, out_rows, out_hi);
+    a.use_cand_count = 1;
+    a.cap = p.cap;
+    RET(launch_select(a, s));
+    prof_record(3, s);
+    int bad = 0;
+    uint64_t cands = 0;
+    RET(read_topk_status(s, &bad, &cands));
+    g.kt.topk_candidates = cands;
+    if (bad) {
+      g.kt.topk_fallback = 1;
+      RET(topk_direct(keys, rows, n, kk, out_rows, out_hi, s));
+      prof_record(3, s);
+      CK(cudaStreamSynchronize(s));
+    }
+  }
+  if (g.prof) {
+    g.kt.topk_threshold_ms = prof_ms(0, 1);
+    g.kt.topk_filter_ms = prof_ms(1, 2);
+    g.kt.topk_select_ms = prof_ms(2, 3);
+  }
+  return GOLP_OK;
+}
+
+// ---- join -------------------------------------------------------------------------
+int grid_for(uint64_t n, int threads, int per_sm) {
+  uint64_t b = (n + threads - 1) / threads;
+  b = std::max<uint64_t>(1, std::min<uint64_t>(b, (uint64_t)g.sms * per_sm));
+  return (int)b;
+}
+
+int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cudaStream_t s) {
+  uint64_t cap = 1024;
+  while (cap < 2 * nb) cap <<= 1;
+  if (cap > (1ull << 32)) {
+    set_error("join build side too large for 32-bit slot indices");
+    return GOLP_ERR_CAPACITY;
+  }
+  CK(g.table.ensure(cap * sizeof(Slot)));
+  const uint64_t nbb = std::max<uint64_t>(nb, 1);
+  CK(g.bslot.ensure(nbb * 4));
+  CK(g.brank.ensure(nbb * 4));
+  CK(g.csr_pos.ensure(nbb * 4));
+  CK(g.csr_row.ensure(nbb * 4));
+  CK(g.big_list.ensure((nbb / (kSmallGroup + 1) + 1) * 4));
+  CK(g.jcount.ensure(16));
+  g.jcap = cap;
+  g.jmask = cap - 1;
+  g.jnb = nb;
+  Slot* table = g.table.as<Slot>();
+  join_init_table_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap);
+  CKL();
+  ++g_launches;
+  CK(cudaMemsetAsync(g.jcount.p, 0, 16, s));
+  if (nb == 0) return GOLP_OK;
+  unsigned long long* cursor = g.jcount.as<unsigned long long>();
+  unsigned int* big_count = reinterpret_cast<unsigned int*>(cursor + 1);
+  const int gb = grid_for(nb, 256, 8);
+  join_insert_kernel<<<gb, 256, 0, s>>>(bkeys, nb, table, g.jmask, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>());
+  CKL();
+  join_offsets_kernel<<<gb, 256, 0, s>>>(nb, table, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>(), cursor,
+                                         g.big_list.as<uint32_t>(), big_count);
+  CKL();
+  join_fill_kernel<<<gb, 256, 0, s>>>(nb, table, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>(),
+                                      g.csr_pos.as<uint32_t>());
+  CKL();
+  join_small_groups_kernel<<<gb, 256, 0, s>>>(nb, table, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>(),
+                                              g.csr_pos.as<uint32_t>(), brows, g.csr_row.as<uint32_t>());
+  CKL();
+  static bool attr = false;
+  const size_t smem = kGroupTile * sizeof(uint32_t);
+  if (!attr) {
+    CK(cudaFuncSetAttribute(join_big_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  join_big_groups_kernel<<<g.sms, 1024, smem, s>>>(table, g.big_list.as<uint32_t>(), big_count,
+                                                   g.csr_pos.as<uint32_t>(), brows, g.csr_row.as<uint32_t>());
+  CKL();
+  g_launches += 5;
+  return GOLP_OK;
+}
+
+// One probe launch over [pkeys, pkeys+np); pair offsets continue from *base_in.
+int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
+                 uint64_t cap, unsigned long long* tile_status, unsigned int* tile_counter,
+                 const unsigned long long* base_in, unsigned long long* total_out, cudaStream_t s) {
+  if (np == 0) {
+    CK(cudaMemcpyAsync(total_out, base_in, 8, cudaMemcpyDeviceToDevice, s));
+    return GOLP_OK;
+  }
+  ProbeArgs a;
+  a.pkeys = pkeys;
+  a.prows = prows;
+  a.np = np;
+  a.table = g.table.as<Slot>();
+  a.mask = g.jmask;
+  a.csr_row = g.csr_row.as<uint32_t>();
+  a.out_p = out_p;
+  a.out_b = out_b;
+  a.cap = cap;
+  a.tile_status = tile_status;
+  a.tile_counter = tile_counter;
+  a.base_in = base_in;
+  a.total_out = total_out;
+  a.ntiles = (np + kProbeTile - 1) / kProbeTile;
+  join_probe_kernel<<<(unsigned)a.ntiles, kProbeThreads, 0, s>>>(a);
+  CKL();
+  ++g_launches;
+  return GOLP_OK;
+}
+
+int ensure_probe_ws(uint64_t ntiles_total, uint64_t launches) {
+  CK(g.tile_status.ensure(std::max<uint64_t>(ntiles_total, 1) * 8));
+  CK(g.tile_counter.ensure(std::max<uint64_t>(launches, 1) * 4));
+  CK(g.totals.ensure((launches + 1) * 8));
+  return GOLP_OK;
+}
+
+int read_u64(const void* dptr, uint64_t* out, cudaStream_t s) {
+  uint64_t* h = static_cast<uint64_t*>(g.pin_small);
+  CK(cudaMemcpyAsync(h, dptr, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *out = *h;
+  return GOLP_OK;
+}
+
+int join_probe_impl(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
+                    uint64_t cap, uint64_t* out_m, cudaStream_t s) {
+  const uint64_t ntiles = (np + kProbeTile - 1) / kProbeTile;
+  RET(ensure_probe_ws(ntiles, 1));
+  CK(cudaMemsetAsync(g.tile_status.p, 0, std::max<uint64_t>(ntiles, 1) * 8, s));
+  CK(cudaMemsetAsync(g.tile_counter.p, 0, 4, s));
+  CK(cudaMemsetAsync(g.totals.p, 0, 16, s));
+  unsigned long long* totals = g.totals.as<unsigned long long>();
+  if (g.jnb > 0) {
+    RET(launch_probe(pkeys, prows, np, out_p, out_b, cap, g.tile_status.as<unsigned long long>(),
+                     g.tile_counter.as<unsigned int>(), totals, totals + 1, s));
+  }
+  RET(read_u64(totals + 1, out_m, s));
+  return GOLP_OK;
+}
+
+cudaStream_t as_stream(void* p) { return p ? static_cast<cudaStream_t>(p) : (cudaStream_t)0; }
+
+int check_mode(int mode, uint32_t payload_bytes, uint64_t* entry) {
+  if (mode == GOLP_KEY_ONLY) {
+    *entry = 12;
+    return GOLP_OK;
+  }
+  if (mode == GOLP_FULL_ROW) {
+    if (payload_bytes < 1) return invalid("full_row transfers need a positive payload_bytes");
+    *entry = 8 + (uint64_t)payload_bytes;
+    return GOLP_OK;
+  }
+  return invalid("unknown transfer mode");
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+const char* golp_last_error(void) { return last_error_cstr(); }
+int golp_version(void) { return 1; }
+
+int golp_init(int device, uint64_t pinned_chunk_bytes, int host_threads) {
+  return do_init(device, pinned_chunk_bytes, host_threads);
+}
+
+int golp_shutdown(void) {
+  if (!g.ready) return GOLP_OK;
+  cudaDeviceSynchronize();
+  g.pool.stop();
+  DevBuf* bufs[] = {&g.ctl, &g.cand_hi, &g.cand_lo, &g.w_hi, &g.w_lo, &g.out_rows, &g.out_hi, &g.samples,
+                    &g.table, &g.bslot, &g.brank, &g.csr_pos, &g.csr_row, &g.big_list, &g.jcount,
+                    &g.tile_status, &g.tile_counter, &g.totals, &g.pairs_p, &g.pairs_b, &g.in_keys, &g.in_rows,
+                    &g.in_bkeys, &g.in_brows, &g.in_payload};
+  for (DevBuf* b : bufs) b->release();
+  for (int i = 0; i < kSlots; ++i) {
+    if (g.pin[i]) cudaFreeHost(g.pin[i]);
+    if (g.pin_ev[i]) cudaEventDestroy(g.pin_ev[i]);
+    g.pin[i] = nullptr;
+    g.pin_ev[i] = nullptr;
+    g.pin_busy[i] = false;
+  }
+  if (g.pin_small) cudaFreeHost(g.pin_small);
+  g.pin_small = nullptr;
+  for (auto& e : g.ev) {
+    if (e) cudaEventDestroy(e);
+    e = nullptr;
+  }
+  cudaStreamDestroy(g.s_main);
+  cudaStreamDestroy(g.s_h2d);
+  cudaStreamDestroy(g.s_d2h);
+  g.jcap = g.jmask = g.jnb = 0;
+  g.last_probe_valid = false;
+  g.ready = false;
+  return GOLP_OK;
+}
+
+uint64_t golp_launch_count(void) { return g_launches.load(); }
+
+int golp_set_profiling(int on) {
+  RET(ensure_init());
+  g.prof = on != 0;
+  return GOLP_OK;
+}
+
+int golp_last_kernel_times(golp_kernel_times* out) {
+  if (!out) return invalid("null output");
+  *out = g.kt;
+  return GOLP_OK;
+}
+
+// ---- device-resident ------------------------------------------------------------------
+int golp_topk_device(const double* d_keys, const uint32_t* d_rows, uint64_t n, uint64_t k, uint32_t* d_out_rows,
+                     uint64_t* d_out_keys, void* stream) {
+  if (k < 1) return invalid("k must be at least 1");
+  RET(ensure_init());
+  if (n > 0 && (!d_keys || !d_rows || !d_out_rows)) return invalid("null device pointer");
+  return topk_device_impl(d_keys, d_rows, n, k, d_out_rows, d_out_keys, as_stream(stream));
+}
+
+int golp_topk_merge_device(const uint64_t* d_key_codes, const uint32_t* d_rows, uint64_t n, uint64_t k,
+                           uint32_t* d_out_rows, uint64_t* d_out_keys, void* stream) {
+  if (k < 1) return invalid("k must be at least 1");
+  RET(ensure_init());
+  const uint64_t kk = std::min(k, n);
+  if (kk == 0) return GOLP_OK;
+  cudaStream_t s = as_stream(stream);
+  RET(ensure_topk_ws(kk, 0));
+  CK(cudaMemsetAsync(ctl(2), 0, sizeof(SelectCtl), s));
+  RET(launch_select(make_args(SrcPairs{d_key_codes, d_rows}, n, kk, kModeFull, 2, d_out_rows, d_out_keys), s));
+  CK(cudaStreamSynchronize(s));
+  return GOLP_OK;
+}
+
+int golp_join_build_device(const double* d_build_keys, const uint32_t* d_build_rows, uint64_t nb, void* stream) {
+  RET(ensure_init());
+  cudaStream_t s = as_stream(stream);
+  prof_record(4, s);
+  RET(join_build_impl(d_build_keys, d_build_rows, nb, s));
+  prof_record(5, s);
+  if (g.prof) {
+    CK(cudaStreamSynchronize(s));
+    g.kt.join_build_ms = prof_ms(4, 5);
+    g.kt.join_capacity = g.jcap;
+  }
+  return GOLP_OK;
+}
+
+int golp_join_probe_device(const double* d_probe_keys, const uint32_t* d_probe_rows, uint64_t np,
+                           uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
+                           uint64_t* out_matches, void* stream) {
+  RET(ensure_init());
+  if (!out_matches) return invalid("null out_matches");
+  cudaStream_t s = as_stream(stream);
+  prof_record(6, s);
+  RET(join_probe_impl(d_probe_keys, d_probe_rows, np, d_out_probe_rows, d_out_build_rows, cap, out_matches, s));
+  prof_record(7, s);
+  if (g.prof) {
+    CK(cudaStreamSynchronize(s));
+    g.kt.join_probe_ms = prof_ms(6, 7);
+  }
+  if (*out_matches > cap) {
+    set_error("probe output exceeds the supplied capacity");
+    return GOLP_ERR_CAPACITY;
+  }
+  return GOLP_OK;
+}
+
+// ---- host buffers (E2E) -----------------------------------------------------------------
+int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, int mode, uint32_t payload_bytes,
+              uint32_t* out_rows, uint64_t* out_len, golp_ledger* led) {
+  if (k < 1) return invalid("k must be at least 1");
+  uint64_t entry = 0;
+  RET(check_mode(mode, payload_bytes, &entry));
+  if (!out_len || !led) return invalid("null output pointer");
+  RET(ensure_init());
+  const double t0 = wall_seconds();
+  const uint64_t kk = std::min(k, n);
+  *out_len = kk;
+  *led = golp_ledger{entry * n, 4 * kk, 0.0, 0.0, 0.0, 0.0};
+  if (n == 0) return GOLP_OK;
+  if (!keys || !rows || !out_rows) return invalid("null buffer");
+  cudaStream_t s = g.s_main;
+  CK(g.in_keys.ensure(n * 8));
+  CK(g.in_rows.ensure(n * 4));
+  CK(g.out_rows.ensure(kk * 4));
+  double* dk = g.in_keys.as<double>();
+  uint32_t* dr = g.in_rows.as<uint32_t>();
+  const TopkPlan p = plan_topk(n, kk);
+  RET(ensure_topk_ws(kk, p.direct ? 0 : p.cap));
+  g.kt.topk_fallback = 0;
+  g.kt.topk_candidates = 0;
+
+  cudaEvent_t ev_chunk = g.ev[0];
+  if (!p.direct) {
+    // Stratified samples gathered on the host (same strata as SrcSample).
+    double* hs = static_cast<double*>(g.pin_small);
+    uint32_t* hr = reinterpret_cast<uint32_t*>(hs + p.s);
+    for (uint64_t i = 0; i < p.s; ++i) {
+      const uint64_t lo = (i * n) / p.s, hi = ((i + 1) * n) / p.s;
+      const uint64_t w = hi > lo ? hi - lo : 1;
+      uint64_t pos = lo + (hash32((uint32_t)i * 2654435761u + 12345u) % w);
+      if (pos >= n) pos = n - 1;
+      hs[i] = keys[pos];
+      hr[i] = rows[pos];
+    }
+    CK(g.samples.ensure(p.s * 12));
+    double* ds = g.samples.as<double>();
+    uint32_t* dsr = reinterpret_cast<uint32_t*>(ds + p.s);
+    CK(cudaMemcpyAsync(ds, hs, p.s * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dsr, hr, p.s * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(ctl(0), 0, sizeof(SelectCtl) * 2, s));
+    RET(launch_select(make_args(SrcInput{ds, dsr}, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), s));
+  }
+  // Stream the columns chunk by chunk; filter each chunk as soon as it lands.
+  const uint64_t per_chunk = std::max<uint64_t>(g.chunk / 8, 1);
+  for (uint64_t c0 = 0; c0 < n; c0 += per_chunk) {
+    const uint64_t cn = std::min(per_chunk, n - c0);
+    RET(stage_h2d(dk + c0, keys + c0, cn * 8));
+    RET(stage_h2d(dr + c0, rows + c0, cn * 4));
+    if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(cn * (size_t)payload_bytes));
+    if (!p.direct) {
+      CK(cudaEventRecord(ev_chunk, g.s_h2d));
+      CK(cudaStreamWaitEvent(s, ev_chunk, 0));
+      RET(launch_filter(dk + c0, dr + c0, cn, p.cap, s));
+    }
+  }
+  CK(cudaEventRecord(ev_chunk, g.s_h2d));
+  CK(cudaEventSynchronize(ev_chunk));
+  g.next_slot = 0;
+  for (bool& b : g.pin_busy) b = false;
+  const double t1 = wall_seconds();
+  CK(cudaStreamWaitEvent(s, ev_chunk, 0));
+  uint32_t* d_out = g.out_rows.as<uint32_t>();
+  if (p.direct) {
+    RET(topk_direct(dk, dr, n, kk, d_out, nullptr, s));
+    CK(cudaStreamSynchronize(s));
+  } else {
+    SelectArgs<SrcCand> a = make_args(SrcCand{g.cand_hi.as<uint64_t>(), g.cand_lo.as<uint32_t>()}, 0, kk,
+                                      kModeFull, 1, d_out, nullptr);
+    a.use_cand_count = 1;
+    a.cap = p.cap;
+    RET(launch_select(a, s));
+    int bad = 0;
+    uint64_t cands = 0;
+    RET(read_topk_status(s, &bad, &cands));
+    g.kt.topk_candidates = cands;
+    if (bad) {
+      g.kt.topk_fallback = 1;
+      RET(topk_direct(dk, dr, n, kk, d_out, nullptr, s));
+      CK(cudaStreamSynchronize(s));
+    }
+  }
+  const double t2 = wall_seconds();
+  uint32_t* hbuf = static_cast<uint32_t*>(g.pin_small);
+  if (kk * 4 <= g.pin_small_bytes) {
+    CK(cudaMemcpyAsync(hbuf, d_out, kk * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::memcpy(out_rows, hbuf, kk * 4);
+  } else {
+    CK(cudaStreamSynchronize(s));
+    RET(stage_d2h(out_rows, d_out, kk * 4));
+  }
+  const double t3 = wall_seconds();
+  led->t_h2d = t1 - t0;
+  led->t_kernel = t2 - t1;
+  led->t_d2h = t3 - t2;
+  return GOLP_OK;
+}
+
+int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb, const double* probe_keys,
+               const uint32_t* probe_rows, uint64_t np, int mode, uint32_t payload_bytes, uint64_t* out_matches,
+               golp_ledger* led) {
+  uint64_t entry = 0;
+  RET(check_mode(mode, payload_bytes, &entry));
+  if (!out_matches || !led) return invalid("null output pointer");
+  RET(ensure_init());
+  g.last_probe_valid = false;
+  const double t0 = wall_seconds();
+  *led = golp_ledger{entry * (nb + np), 0, 0.0, 0.0, 0.0, 0.0};
+  *out_matches = 0;
+  if ((nb && (!build_keys || !build_rows)) || (np && (!probe_keys || !probe_rows))) return invalid("null buffer");
+  cudaStream_t s = g.s_main;
+  CK(g.in_bkeys.ensure(std::max<uint64_t>(nb, 1) * 8));
+  CK(g.in_brows.ensure(std::max<uint64_t>(nb, 1) * 4));
+  CK(g.in_keys.ensure(std::max<uint64_t>(np, 1) * 8));
+  CK(g.in_rows.ensure(std::max<uint64_t>(np, 1) * 4));
+  double* dbk = g.in_bkeys.as<double>();
+  uint32_t* dbr = g.in_brows.as<uint32_t>();
+  double* dpk = g.in_keys.as<double>();
+  uint32_t* dpr = g.in_rows.as<uint32_t>();
+
+  // build side first, then the probe side in chunks that are probed as they land
+  RET(stage_h2d(dbk, build_keys, nb * 8));
+  RET(stage_h2d(dbr, build_rows, nb * 4));
+  if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(nb * (size_t)payload_bytes));
+  cudaEvent_t ev_chunk = g.ev[0];
+  CK(cudaEventRecord(ev_chunk, g.s_h2d));
+  CK(cudaStreamWaitEvent(s, ev_chunk, 0));
+  RET(join_build_impl(dbk, dbr, nb, s));
+
+  uint64_t per_chunk = std::max<uint64_t>(g.chunk / 8, kProbeTile);
+  per_chunk = (per_chunk / kProbeTile) * kProbeTile;
+  const uint64_t nchunks = np ? (np + per_chunk - 1) / per_chunk : 0;
+  const uint64_t ntiles_total = (np + kProbeTile - 1) / kProbeTile + nchunks;
+  RET(ensure_probe_ws(ntiles_total, nchunks));
+  CK(cudaMemsetAsync(g.tile_status.p, 0, std::max<uint64_t>(ntiles_total, 1) * 8, s));
+  CK(cudaMemsetAsync(g.tile_counter.p, 0, std::max<uint64_t>(nchunks, 1) * 4, s));
+  CK(cudaMemsetAsync(g.totals.p, 0, (nchunks + 1) * 8, s));
+  uint64_t out_cap = std::max<uint64_t>(g.pairs_p.bytes / 4, std::max<uint64_t>(np, 1024));
+  CK(g.pairs_p.ensure(out_cap * 4));
+  CK(g.pairs_b.ensure(out_cap * 4));
+  out_cap = std::min(g.pairs_p.bytes, g.pairs_b.bytes) / 4;
+  unsigned long long* totals = g.totals.as<unsigned long long>();
+  auto run_chunks = [&](bool with_h2d) -> int {
+    uint64_t tile_off = 0;
+    for (uint64_t c = 0; c < nchunks; ++c) {
+      const uint64_t c0 = c * per_chunk;
+      const uint64_t cn = std::min(per_chunk, np - c0);
+      if (with_h2d) {
+        RET(stage_h2d(dpk + c0, probe_keys + c0, cn * 8));
+        RET(stage_h2d(dpr + c0, probe_rows + c0, cn * 4));
+        if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(cn * (size_t)payload_bytes));
+        CK(cudaEventRecord(ev_chunk, g.s_h2d));
+        CK(cudaStreamWaitEvent(s, ev_chunk, 0));
+      }
+      if (g.jnb > 0) {
+        RET(launch_probe(dpk + c0, dpr + c0, cn, g.pairs_p.as<uint32_t>(), g.pairs_b.as<uint32_t>(), out_cap,
+                         g.tile_status.as<unsigned long long>() + tile_off, g.tile_counter.as<unsigned int>() + c,
+                         totals + c, totals + c + 1, s));
+      } else {
+        CK(cudaMemsetAsync(totals + c + 1, 0, 8, s));
+      }
+      tile_off += (cn + kProbeTile - 1) / kProbeTile;
+    }
+    return GOLP_OK;
+  };
+  RET(run_chunks(true));
+  CK(cudaEventRecord(ev_chunk, g.s_h2d));
+  CK(cudaEventSynchronize(ev_chunk));
+  g.next_slot = 0;
+  for (bool& b : g.pin_busy) b = false;
+  const double t1 = wall_seconds();
+  uint64_t m = 0;
+  RET(read_u64(totals + nchunks, &m, s));
+  if (m > out_cap) {  // rare: more pairs than probes; grow and re-probe the resident input
+    CK(g.pairs_p.ensure(m * 4));
+    CK(g.pairs_b.ensure(m * 4));
+    out_cap = std::min(g.pairs_p.bytes, g.pairs_b.bytes) / 4;
+    CK(cudaMemsetAsync(g.tile_status.p, 0, std::max<uint64_t>(ntiles_total, 1) * 8, s));
+    CK(cudaMemsetAsync(g.tile_counter.p, 0, std::max<uint64_t>(nchunks, 1) * 4, s));
+    CK(cudaMemsetAsync(g.totals.p, 0, (nchunks + 1) * 8, s));
+    RET(run_chunks(false));
+    RET(read_u64(totals + nchunks, &m, s));
+  }
+  const double t2 = wall_seconds();
+  *out_matches = m;
+  g.last_m = m;
+  g.last_probe_valid = true;
+  led->t_h2d = t1 - t0;
+  led->t_kernel = t2 - t1;
+  return GOLP_OK;
+}
+
+int golp_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m, golp_ledger* led) {
+  if (!g.last_probe_valid) return invalid("no probe result to copy out");
+  if (m != g.last_m) return invalid("copy_out size does not match the last probe's match count");
+  const double t0 = wall_seconds();
+  if (m) {
+    if (!probe_rows || !build_rows) return invalid("null buffer");
+    RET(stage_d2h(probe_rows, g.pairs_p.p, m * 4));
+    RET(stage_d2h(build_rows, g.pairs_b.p, m * 4));
+  }
+  RET(sync_ring());
+  if (led) {
+    led->d2h_bytes = 8 * m;
+    led->t_d2h = wall_seconds() - t0;
+  }
+  return GOLP_OK;
+}
+
+}  // extern "C"

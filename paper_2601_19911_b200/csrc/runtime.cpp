@@ -1,0 +1,92 @@
+#include "runtime.h"
+
+namespace golp {
+
+static std::mutex g_err_mu;
+static std::string g_err;
+
+void set_error(const std::string& msg) {
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  g_err = msg;
+}
+
+const char* last_error_cstr() {
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  return g_err.c_str();
+}
+
+double wall_seconds() {
+  using clk = std::chrono::steady_clock;
+  return std::chrono::duration<double>(clk::now().time_since_epoch()).count();
+}
+
+void WorkerPool::start(int workers) {
+  stop();
+  stop_ = false;
+  for (int i = 0; i < workers; ++i) threads_.emplace_back([this] { loop(); });
+}
+
+void WorkerPool::stop() {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    stop_ = true;
+  }
+  cv_work_.notify_all();
+  for (auto& t : threads_) t.join();
+  threads_.clear();
+}
+
+void WorkerPool::loop() {
+  uint64_t seen = 0;
+  while (true) {
+    const std::function<void(size_t)>* job;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_work_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      job = job_;
+    }
+    for (size_t i = next_.fetch_add(1); i < total_; i = next_.fetch_add(1)) (*job)(i);
+    std::lock_guard<std::mutex> lk(mu_);
+    if (--pending_ == 0) cv_done_.notify_all();
+  }
+}
+
+void WorkerPool::run(size_t ntasks, const std::function<void(size_t)>& fn) {
+  if (threads_.empty() || ntasks <= 1) {
+    for (size_t i = 0; i < ntasks; ++i) fn(i);
+    return;
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    job_ = &fn;
+    total_ = ntasks;
+    next_.store(0);
+    pending_ = (int)threads_.size();
+    ++gen_;
+  }
+  cv_work_.notify_all();
+  for (size_t i = next_.fetch_add(1); i < ntasks; i = next_.fetch_add(1)) fn(i);
+  std::unique_lock<std::mutex> lk(mu_);
+  cv_done_.wait(lk, [&] { return pending_ == 0; });
+}
+
+void parallel_copy(WorkerPool& pool, void* dst, const void* src, size_t bytes) {
+  constexpr size_t kPiece = 2u << 20;
+  const size_t pieces = (bytes + kPiece - 1) / kPiece;
+  if (pieces <= 1 || pool.size() == 0) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t tasks = std::min(pieces, (size_t)pool.size() + 1);
+  const size_t per = (bytes + tasks - 1) / tasks;
+  pool.run(tasks, [&](size_t t) {
+    const size_t lo = t * per;
+    if (lo >= bytes) return;
+    const size_t len = std::min(per, bytes - lo);
+    std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, len);
+  });
+}
+
+}  // namespace golp

@@ -1,0 +1,436 @@
+// Top-K selection over (key f64, row u32) pairs: the B200 replacement for the
+// reference's data-parallel Top-K (ProxyDevice.topk -> _chunk_topk_candidates +
+// _merge_topk_candidates, pkg/src/golp/device.py:239-259,329-380), bit-exact with
+// host_topk (pkg/src/golp/host.py:133-144): the k largest keys, descending, equal
+// keys by ascending row id.
+//
+// Order: composite item (hi = ord(key), lo = ~row), larger is better.
+//
+// Pipeline (one read of the key column on the common path):
+//   1. threshold  : radix-select the r-th best of S stratified samples (THRESH mode
+//                   of the select engine) -> conservative composite threshold T.
+//   2. filter     : stream keys with 128-bit loads, keep items >= T (warp-aggregated
+//                   appends), rows are gathered only for survivors.
+//   3. select     : MSB radix select over the candidates (smem histograms, 8-bit
+//                   digits, one grid barrier per digit) -> exact K-th item, then
+//                   collect the K winners and bitonic-sort them (one block when
+//                   K <= 8192, otherwise a grid-wide network with smem tiles).
+// If the sampled threshold admits fewer than K or more than `cap` candidates the
+// host re-runs step 3 directly over the input (exact, slower, never wrong).
+#pragma once
+#include <cooperative_groups.h>
+#include "sortnet.cuh"
+
+namespace golp {
+
+namespace cg = cooperative_groups;
+
+constexpr int kSelThreads = 1024;
+constexpr uint32_t kSortTile = 8192;  // items per shared-memory sort tile (96 KB)
+constexpr int kModeFull = 0;          // radix select + collect + sort + emit
+constexpr int kModeThreshold = 1;     // radix select only -> ctl->thr_*
+
+struct SelectCtl {
+  unsigned int hist[12][256];
+  unsigned long long cand_count;  // filter output (may exceed cap: overflow)
+  unsigned long long win_count;
+  unsigned long long eq_count;
+  double thr_key;
+  uint32_t thr_row;
+  int status;  // 0 ok, 1 candidate set unusable (host falls back to direct)
+  unsigned long long res_hi;
+  uint32_t res_lo;
+  int res_bits;
+};
+
+// ---- item sources -------------------------------------------------------------
+
+struct SrcInput {  // the caller's (keys, rows) columns
+  const double* keys;
+  const uint32_t* rows;
+  __device__ __forceinline__ uint64_t hi(uint64_t i) const { return ord_key(__ldg(keys + i)); }
+  __device__ __forceinline__ uint32_t lo(uint64_t i) const { return ~__ldg(rows + i); }
+};
+
+struct SrcCand {  // encoded candidate arrays written by the filter (or a merge)
+  const uint64_t* h;
+  const uint32_t* l;
+  __device__ __forceinline__ uint64_t hi(uint64_t i) const { return __ldcg(h + i); }
+  __device__ __forceinline__ uint32_t lo(uint64_t i) const { return __ldcg(l + i); }
+};
+
+struct SrcPairs {  // encoded keys + plain row ids (all-gathered local Top-K results)
+  const uint64_t* h;
+  const uint32_t* rows;
+  __device__ __forceinline__ uint64_t hi(uint64_t i) const { return __ldcg(h + i); }
+  __device__ __forceinline__ uint32_t lo(uint64_t i) const { return ~__ldcg(rows + i); }
+};
+
+// S stratified samples of an n-item column: sample i comes from stratum
+// [i*n/S, (i+1)*n/S) at a hashed offset, so periodic layouts cannot alias.
+struct SrcSample {
+  const double* keys;
+  const uint32_t* rows;
+  uint64_t n;
+  uint64_t s;
+  __device__ __forceinline__ uint64_t pos(uint64_t i) const {
+    const uint64_t lo_ = (i * n) / s;
+    const uint64_t hi_ = ((i + 1) * n) / s;
+    const uint64_t w = hi_ > lo_ ? hi_ - lo_ : 1;
+    uint64_t p = lo_ + (hash32((uint32_t)i * 2654435761u + 12345u) % w);
+    return p < n ? p : n - 1;
+  }
+  __device__ __forceinline__ uint64_t hi(uint64_t i) const { return ord_key(__ldg(keys + pos(i))); }
+  __device__ __forceinline__ uint32_t lo(uint64_t i) const { return ~__ldg(rows + pos(i)); }
+};
+
+template <class Src>
+struct SelectArgs {
+  Src src;
+  uint64_t n;          // items in src (ignored when use_cand_count)
+  uint64_t need;       // K' (items wanted), 1 <= need
+  uint64_t cap;        // candidate capacity (use_cand_count only)
+  int use_cand_count;  // n := ctl->cand_count, validated against need/cap
+  int mode;
+  SelectCtl* ctl;
+  uint64_t* w_hi;      // winners scratch, >= need entries
+  uint32_t* w_lo;
+  uint32_t* out_rows;  // need entries, best first
+  uint64_t* out_hi;    // optional: encoded keys of the winners (for merges)
+};
+
+// Compare the top `bits` bits of (h, l) against the prefix: -1, 0, +1.
+__device__ __forceinline__ int prefix_cmp(uint64_t h, uint32_t l, uint64_t ph, uint32_t pl, int bits) {
+  if (bits <= 0) return 0;
+  if (bits <= 64) {
+    const int sh = 64 - bits;
+    const uint64_t a = sh >= 64 ? 0 : (h >> sh), b = sh >= 64 ? 0 : (ph >> sh);
+    return a > b ? 1 : (a < b ? -1 : 0);
+  }
+  if (h != ph) return h > ph ? 1 : -1;
+  const int sh = 96 - bits;
+  const uint32_t a = l >> sh, b = pl >> sh;
+  return a > b ? 1 : (a < b ? -1 : 0);
+}
+
+template <class Src>
+__global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs<Src> a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* s_hi = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* s_lo = reinterpret_cast<uint32_t*>(s_hi + kSortTile);
+  __shared__ unsigned s_hist[256];
+  __shared__ uint64_t sh_pre_hi;
+  __shared__ uint32_t sh_pre_lo;
+  __shared__ int sh_bits;
+  __shared__ unsigned long long sh_rem;
+  __shared__ int sh_done;
+
+  const Src src = a.src;
+  uint64_t n = a.n;
+  if (a.use_cand_count) {
+    const unsigned long long c = *(volatile unsigned long long*)&a.ctl->cand_count;
+    if (c > a.cap || c < a.need) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->status = 1;
+      return;  // uniform across the grid: no barrier is ever reached
+    }
+    n = c;
+  }
+  const uint64_t need = a.need < n ? a.need : n;
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+
+  // Small lists: one block sorts everything and emits the best `need`.
+  if (a.mode == kModeFull && n <= kSortTile) {
+    if (blockIdx.x != 0) return;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      s_hi[i] = src.hi(i);
+      s_lo[i] = src.lo(i);
+    }
+    __syncthreads();
+    block_sort_desc(s_hi, s_lo, (uint32_t)n);
+    for (uint32_t i = threadIdx.x; i < need; i += blockDim.x) {
+      a.out_rows[i] = ~s_lo[i];
+      if (a.out_hi) a.out_hi[i] = s_hi[i];
+    }
+    return;
+  }
+
+  // ---- MSB radix select on the 96-bit composite, 8-bit digits ----------------
+  uint64_t pre_hi = 0;
+  uint32_t pre_lo = 0;
+  int bits = 0;
+  uint64_t rem = need;
+  for (int pass = 0; pass < 12; ++pass) {
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) s_hist[t] = 0;
+    __syncthreads();
+    for (uint64_t i = gtid; i < n; i += gstride) {
+      const uint64_t h = src.hi(i);
+      unsigned d;
+      if (bits < 64) {
+        if (bits > 0 && (h >> (64 - bits)) != (pre_hi >> (64 - bits))) continue;
+        d = (unsigned)(h >> (56 - bits)) & 255u;
+      } else {
+        if (h != pre_hi) continue;
+        const uint32_t l = src.lo(i);
+        if (bits > 64 && (l >> (96 - bits)) != (pre_lo >> (96 - bits))) continue;
+        d = (l >> (24 - (bits - 64))) & 255u;
+      }
+      atomicAdd(&s_hist[d], 1u);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 256; t += blockDim.x)
+      if (s_hist[t]) atomicAdd(&a.ctl->hist[pass][t], s_hist[t]);
+    grid.sync();
+    // Every block resolves the digit identically from the global histogram.
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      unsigned c8[8];
+      unsigned long long lsum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {  // lane covers bins 255-8*lane-q (descending)
+        c8[q] = __ldcg(&a.ctl->hist[pass][255 - 8 * lane - q]);
+        lsum += c8[q];
+      }
+      unsigned long long incl = lsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const unsigned long long excl = incl - lsum;
+      const bool mine = excl < rem && incl >= rem;
+      if (mine) {
+        unsigned long long cum = excl;
+        int b = -1;
+        unsigned cb = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (b < 0 && cum + c8[q] >= rem) { b = 255 - 8 * lane - q; cb = c8[q]; }
+          else if (b < 0) cum += c8[q];
+        }
+        const uint64_t new_rem = rem - cum;
+        uint64_t ph = pre_hi;
+        uint32_t pl = pre_lo;
+        if (bits < 64) ph |= (uint64_t)b << (56 - bits);
+        else pl |= (uint32_t)b << (24 - (bits - 64));
+        sh_pre_hi = ph;
+        sh_pre_lo = pl;
+        sh_bits = bits + 8;
+        sh_rem = new_rem;
+        sh_done = (new_rem == cb) || (bits + 8 >= 96);
+      }
+    }
+    __syncthreads();
+    pre_hi = sh_pre_hi;
+    pre_lo = sh_pre_lo;
+    bits = sh_bits;
+    rem = sh_rem;
+    const int done = sh_done;
+    __syncthreads();
+    if (done) break;
+  }
+
+  if (a.mode == kModeThreshold) {
+    // Everything >= (pre_hi, pre_lo) (low bits zero) holds the `need` best samples.
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.ctl->thr_key = key_from_ord(pre_hi);
+      a.ctl->thr_row = ~pre_lo;
+      a.ctl->res_hi = pre_hi;
+      a.ctl->res_lo = pre_lo;
+      a.ctl->res_bits = bits;
+    }
+    return;
+  }
+
+  // ---- collect exactly `need` winners ----------------------------------------
+  for (uint64_t wb = gtid - lane_id(); wb < n; wb += gstride) {
+    const uint64_t i = wb + lane_id();
+    bool take = false;
+    uint64_t h = 0;
+    uint32_t l = 0;
+    if (i < n) {
+      h = src.hi(i);
+      l = (bits > 64 || h >= pre_hi) ? src.lo(i) : 0u;
+      const int c = prefix_cmp(h, l, pre_hi, pre_lo, bits);
+      if (c > 0) take = true;
+      else if (c == 0) take = bits < 96 || atomicAdd(&a.ctl->eq_count, 1ull) < rem;
+    }
+    const unsigned long long slot = warp_append(&a.ctl->win_count, take);
+    if (take) {
+      __stcg(a.w_hi + slot, h);
+      __stcg(a.w_lo + slot, l);
+    }
+  }
+  grid.sync();
+
+  // ---- sort the winners (best first) and emit -------------------------------
+  if (need <= kSortTile) {
+    if (blockIdx.x != 0) return;
+    for (uint32_t i = threadIdx.x; i < need; i += blockDim.x) {
+      s_hi[i] = __ldcg(a.w_hi + i);
+      s_lo[i] = __ldcg(a.w_lo + i);
+    }
+    __syncthreads();
+    block_sort_desc(s_hi, s_lo, (uint32_t)need);
+    for (uint32_t i = threadIdx.x; i < need; i += blockDim.x) {
+      a.out_rows[i] = ~s_lo[i];
+      if (a.out_hi) a.out_hi[i] = s_hi[i];
+    }
+    return;
+  }
+
+  uint64_t* gh = a.w_hi;
+  uint32_t* gl = a.w_lo;
+  const uint64_t m = need;
+  const uint64_t ntiles = (m + kSortTile - 1) / kSortTile;
+  const int logTile = ilog2_u64(kSortTile);
+  // (a) every tile sorted locally = all merge sizes up to kSortTile
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t base = tile * kSortTile;
+    const uint32_t cnt = (uint32_t)((m - base) < kSortTile ? (m - base) : kSortTile);
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      s_hi[i] = __ldcg(gh + base + i);
+      s_lo[i] = __ldcg(gl + base + i);
+    }
+    __syncthreads();
+    block_sort_desc(s_hi, s_lo, cnt);
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      __stcg(gh + base + i, s_hi[i]);
+      __stcg(gl + base + i, s_lo[i]);
+    }
+    __syncthreads();
+  }
+  grid.sync();
+  const int logP = ilog2_u64(next_pow2_u64(m));
+  const uint64_t pairs = (1ull << logP) >> 1;
+  for (int logk = logTile + 1; logk <= logP; ++logk) {
+    for (uint64_t t = gtid; t < pairs; t += gstride) {
+      uint64_t i, j;
+      flip_pair(t, logk, i, j);
+      if (j < m) {
+        const uint64_t hi_ = __ldcg(gh + i), hj = __ldcg(gh + j);
+        const uint32_t li = __ldcg(gl + i), lj = __ldcg(gl + j);
+        if (item_gt(hj, lj, hi_, li)) {
+          __stcg(gh + i, hj); __stcg(gh + j, hi_);
+          __stcg(gl + i, lj); __stcg(gl + j, li);
+        }
+      }
+    }
+    grid.sync();
+    for (int logs = logk - 2; logs >= logTile; --logs) {
+      for (uint64_t t = gtid; t < pairs; t += gstride) {
+        uint64_t i, j;
+        half_pair(t, logs, i, j);
+        if (j < m) {
+          const uint64_t hi_ = __ldcg(gh + i), hj = __ldcg(gh + j);
+          const uint32_t li = __ldcg(gl + i), lj = __ldcg(gl + j);
+          if (item_gt(hj, lj, hi_, li)) {
+            __stcg(gh + i, hj); __stcg(gh + j, hi_);
+            __stcg(gl + i, lj); __stcg(gl + j, li);
+          }
+        }
+      }
+      grid.sync();
+    }
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const uint64_t base = tile * kSortTile;
+      const uint32_t cnt = (uint32_t)((m - base) < kSortTile ? (m - base) : kSortTile);
+      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+        s_hi[i] = __ldcg(gh + base + i);
+        s_lo[i] = __ldcg(gl + base + i);
+      }
+      __syncthreads();
+      block_half_steps_desc(s_hi, s_lo, cnt, logTile - 1, kSortTile / 2);
+      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+        __stcg(gh + base + i, s_hi[i]);
+        __stcg(gl + base + i, s_lo[i]);
+      }
+      __syncthreads();
+    }
+    grid.sync();
+  }
+  for (uint64_t i = gtid; i < m; i += gstride) {
+    a.out_rows[i] = ~__ldcg(gl + i);
+    if (a.out_hi) a.out_hi[i] = __ldcg(gh + i);
+  }
+}
+
+// ---- streaming filter ------------------------------------------------------------
+// Keeps every item with (key, row) >= (thr_key, thr_row) in Top-K order, i.e.
+// key > thr_key, or key == thr_key and row <= thr_row. Float compare gives the
+// reference's -0.0 == +0.0 for free. Rows are loaded only for survivors and for
+// exact threshold ties.
+constexpr int kFilterThreads = 256;
+constexpr int kFilterUnroll = 4;  // 4 x 16 B loads in flight per thread
+
+__device__ __forceinline__ bool filter_keep(double k, double tk, uint32_t tr, const uint32_t* rows, uint64_t pos) {
+  if (k > tk) return true;
+  if (k == tk) return __ldg(rows + pos) <= tr;
+  return false;
+}
+
+__global__ void __launch_bounds__(kFilterThreads) topk_filter_kernel(
+    const double* __restrict__ keys, const uint32_t* __restrict__ rows, uint64_t n, const SelectCtl* thr,
+    unsigned long long* cand_count, uint64_t* __restrict__ cand_hi, uint32_t* __restrict__ cand_lo,
+    uint64_t cap) {
+  const double tk = *(const volatile double*)&thr->thr_key;
+  const uint32_t tr = *(const volatile uint32_t*)&thr->thr_row;
+  const uint64_t head = (((uintptr_t)keys & 15) != 0 && n > 0) ? 1 : 0;
+  const uint64_t nv = (n - head) / 2;
+  const uint64_t tail = head + 2 * nv;  // index of a leftover odd element (if < n)
+  const double* kv = keys + head;
+  const unsigned lane = lane_id();
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // scalar head / tail elements
+    uint64_t pos = ~0ull;
+    if (lane == 0 && head) pos = 0;
+    if (lane == 1 && tail < n) pos = tail;
+    bool take = false;
+    if (pos != ~0ull) take = filter_keep(keys[pos], tk, tr, rows, pos);
+    const unsigned long long slot = warp_append(cand_count, take);
+    if (take && slot < cap) {
+      cand_hi[slot] = ord_key(keys[pos]);
+      cand_lo[slot] = ~rows[pos];
+    }
+  }
+
+  for (uint64_t wb = gtid - lane; wb < nv; wb += stride * kFilterUnroll) {
+    double2 v[kFilterUnroll];
+#pragma unroll
+    for (int u = 0; u < kFilterUnroll; ++u) {
+      const uint64_t vi = wb + lane + (uint64_t)u * stride;
+      if (vi < nv) v[u] = ldg_nc_d2(kv + 2 * vi);
+      else v[u] = make_double2(-__longlong_as_double(0x7FF0000000000000ll), 0.0);
+    }
+    unsigned flags = 0;
+#pragma unroll
+    for (int u = 0; u < kFilterUnroll; ++u) {
+      const uint64_t vi = wb + lane + (uint64_t)u * stride;
+      if (vi < nv) {
+        const uint64_t p = head + 2 * vi;
+        if (filter_keep(v[u].x, tk, tr, rows, p)) flags |= 1u << (2 * u);
+        if (filter_keep(v[u].y, tk, tr, rows, p + 1)) flags |= 2u << (2 * u);
+      }
+    }
+    if (__any_sync(0xFFFFFFFFu, flags != 0)) {
+#pragma unroll
+      for (int u = 0; u < kFilterUnroll; ++u) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool take = (flags >> (2 * u + e)) & 1u;
+          const unsigned long long slot = warp_append(cand_count, take);
+          if (take && slot < cap) {
+            const uint64_t p = head + 2 * (wb + lane + (uint64_t)u * stride) + e;
+            cand_hi[slot] = ord_key(e ? v[u].y : v[u].x);
+            cand_lo[slot] = ~__ldg(rows + p);
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace golp

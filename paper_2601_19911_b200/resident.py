@@ -1,0 +1,102 @@
+"""Device-resident entry points over torch CUDA tensors (inputs already in HBM).
+
+PyTorch is only plumbing here (allocation, the current stream, and
+torch.distributed in sharded.py); every kernel is libgolp_b200's. Row ids are
+carried in int32 tensors and reinterpreted as u32 by the library.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native
+
+
+def _stream(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _check_cols(keys: torch.Tensor, rows: torch.Tensor) -> None:
+    if keys.dtype != torch.float64 or rows.dtype not in (torch.int32, torch.uint32):
+        raise ValueError("keys must be float64 and rows int32/uint32 tensors")
+    if keys.shape != rows.shape or keys.dim() != 1:
+        raise ValueError("keys and rows must be 1-D tensors of equal length")
+    if not (keys.is_cuda and rows.is_cuda and keys.is_contiguous() and rows.is_contiguous()):
+        raise ValueError("keys and rows must be contiguous CUDA tensors")
+
+
+def topk(keys: torch.Tensor, rows: torch.Tensor, k: int, stream=None, want_codes: bool = False):
+    """Top-k of device-resident (key, row) columns -> (rows[min(k,n)], codes|None).
+
+    codes are the order-preserving u64 key codes (int64 storage) of the winners,
+    the input of `merge` for cross-GPU reductions.
+    """
+    if k < 1:
+        raise ValueError("k must be at least 1")
+    _check_cols(keys, rows)
+    n = keys.numel()
+    kk = min(k, n)
+    out = torch.empty(kk, dtype=torch.int32, device=keys.device)
+    codes = torch.empty(kk, dtype=torch.int64, device=keys.device) if want_codes else None
+    lib = _native.load()
+    _native.check(lib.golp_topk_device(keys.data_ptr(), rows.data_ptr(), n, k, out.data_ptr() if kk else 0,
+                                       codes.data_ptr() if (codes is not None and kk) else 0, _stream(stream)))
+    return out, codes
+
+
+def merge(codes: torch.Tensor, rows: torch.Tensor, k: int, stream=None, want_codes: bool = False):
+    """Exact Top-k of already-encoded candidates (e.g. all-gathered local results)."""
+    if k < 1:
+        raise ValueError("k must be at least 1")
+    n = codes.numel()
+    kk = min(k, n)
+    out = torch.empty(kk, dtype=torch.int32, device=codes.device)
+    oc = torch.empty(kk, dtype=torch.int64, device=codes.device) if want_codes else None
+    lib = _native.load()
+    _native.check(lib.golp_topk_merge_device(codes.data_ptr(), rows.data_ptr(), n, k, out.data_ptr() if kk else 0,
+                                             oc.data_ptr() if (oc is not None and kk) else 0, _stream(stream)))
+    return out, oc
+
+
+def join_build(keys: torch.Tensor, rows: torch.Tensor, stream=None) -> None:
+    _check_cols(keys, rows)
+    _native.check(_native.load().golp_join_build_device(keys.data_ptr(), rows.data_ptr(), keys.numel(),
+                                                        _stream(stream)))
+
+
+def join_probe(keys: torch.Tensor, rows: torch.Tensor, out_probe: torch.Tensor, out_build: torch.Tensor,
+               stream=None) -> int:
+    """Probe the last built table into caller buffers; returns the match count M.
+    Raises CapacityError (pairs truncated) when M exceeds the buffers."""
+    _check_cols(keys, rows)
+    cap = min(out_probe.numel(), out_build.numel())
+    m = C.c_uint64(0)
+    _native.check(_native.load().golp_join_probe_device(keys.data_ptr(), rows.data_ptr(), keys.numel(),
+                                                        out_probe.data_ptr(), out_build.data_ptr(), cap,
+                                                        C.byref(m), _stream(stream)))
+    return int(m.value)
+
+
+def join(bkeys, brows, pkeys, prows, capacity: int | None = None, stream=None):
+    """Build + probe -> (probe_rows[M], build_rows[M]) int32 tensors."""
+    join_build(bkeys, brows, stream)
+    cap = capacity if capacity is not None else max(pkeys.numel(), 1024)
+    while True:
+        op = torch.empty(cap, dtype=torch.int32, device=pkeys.device)
+        ob = torch.empty(cap, dtype=torch.int32, device=pkeys.device)
+        m = C.c_uint64(0)
+        lib = _native.load()
+        rc = lib.golp_join_probe_device(pkeys.data_ptr(), prows.data_ptr(), pkeys.numel(), op.data_ptr(),
+                                        ob.data_ptr(), cap, C.byref(m), _stream(stream))
+        if rc == _native.GOLP_ERR_CAPACITY:
+            cap = int(m.value)
+            continue
+        _native.check(rc)
+        return op[: m.value], ob[: m.value]
+
+
+def set_profiling(on: bool) -> None:
+    _native.check(_native.load().golp_set_profiling(1 if on else 0))

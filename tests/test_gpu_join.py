@@ -1,0 +1,100 @@
+"""B200 hash join parity: reference golden vectors, then seeded instances vs
+the oracle. Pair ORDER is checked (probe position, then build insertion), which
+is stricter than BASELINE's multiset criterion."""
+
+import numpy as np
+import pytest
+
+from golden_io import cases
+from oracle import oracle
+from paper_2601_19911_b200 import FULL_ROW, KeyVector
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", cases("probe"), ids=lambda c: f"{c['tag']}-{len(c['bkeys'])}x{len(c['pkeys'])}")
+def test_probe_matches_reference_golden(b200, case):
+    res = b200.probe(KeyVector(case["bkeys"], case["brows"]), KeyVector(case["pkeys"], case["prows"]))
+    assert res.payload.probe_rows.tolist() == case["exp_p"].tolist()
+    assert res.payload.build_rows.tolist() == case["exp_b"].tolist()
+    assert res.payload.probe_count == len(case["pkeys"])
+    assert res.ledger.h2d_bytes == 12 * (len(case["bkeys"]) + len(case["pkeys"]))
+    assert res.ledger.d2h_bytes == 8 * len(case["exp_p"])
+
+
+@pytest.mark.parametrize("nb,np_,domain", [
+    (1_000_000, 10_000_000, 2_000_000),   # config C2 shape
+    (100_000, 1_000_000, 200_000),
+    (50_000, 300_000, 5_000),             # groups of ~10
+    (200_000, 100_000, 300),              # groups of ~670 (block sort path)
+    (60_000, 5_000, 2),                   # groups of ~30000 (global in-place sort path)
+    (1, 100_000, 2),
+    (100_000, 1, 2),
+])
+def test_probe_random_vs_oracle(b200, nb, np_, domain):
+    rng = np.random.default_rng(nb + np_ + domain)
+    bk = rng.integers(0, domain, size=nb).astype(np.float64)
+    pk = rng.integers(0, domain, size=np_).astype(np.float64)
+    br = rng.permutation(nb).astype(np.uint32)
+    pr = rng.permutation(np_).astype(np.uint32)
+    res = b200.probe(KeyVector(bk, br), KeyVector(pk, pr))
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert np.array_equal(res.payload.probe_rows, ep)
+    assert np.array_equal(res.payload.build_rows, eb)
+
+
+def test_probe_more_pairs_than_probes_grows_output(b200):
+    rng = np.random.default_rng(4)
+    bk = rng.integers(0, 4, size=20_000).astype(np.float64)  # ~5000 matches per probe
+    pk = rng.integers(0, 4, size=3000).astype(np.float64)
+    br = np.arange(20_000, dtype=np.uint32)
+    pr = np.arange(3000, dtype=np.uint32)
+    res = b200.probe(KeyVector(bk, br), KeyVector(pk, pr))
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert res.payload.match_count == len(ep) > 3000
+    assert np.array_equal(res.payload.probe_rows, ep) and np.array_equal(res.payload.build_rows, eb)
+
+
+def test_probe_signed_zero_negative_and_extreme_keys(b200):
+    bk = np.array([0.0, -0.0, -1e300, 1e300, 5e-324, -5e-324, -7.25, 0.0])
+    pk = np.array([-0.0, 1e300, -7.25, 5e-324, 3.0, 0.0])
+    br = np.arange(len(bk), dtype=np.uint32) * 3
+    pr = np.arange(len(pk), dtype=np.uint32) + 100
+    res = b200.probe(KeyVector(bk, br), KeyVector(pk, pr))
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert res.payload.matches == list(zip(ep.tolist(), eb.tolist()))
+
+
+def test_probe_full_row_mode(b200):
+    rng = np.random.default_rng(3)
+    b = KeyVector(rng.integers(0, 100, size=5000).astype(np.float64), np.arange(5000))
+    p = KeyVector(rng.integers(0, 100, size=20_000).astype(np.float64), np.arange(20_000))
+    full = b200.probe(b, p, mode=FULL_ROW, payload_bytes=188)
+    key = b200.probe(b, p)
+    assert full.payload.matches == key.payload.matches
+    assert full.ledger.h2d_bytes == 196 * 25_000
+
+
+def test_join_resident_api(cuda):
+    import torch
+
+    from paper_2601_19911_b200 import resident
+
+    rng = np.random.default_rng(11)
+    nb, np_ = 300_000, 2_000_000
+    bk = rng.integers(0, 600_000, size=nb).astype(np.float64)
+    pk = rng.integers(0, 600_000, size=np_).astype(np.float64)
+    br = rng.permutation(nb).astype(np.uint32)
+    pr = rng.permutation(np_).astype(np.uint32)
+    t = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(cuda)  # noqa: E731
+    op, ob = resident.join(t(bk), t(br), t(pk), t(pr))
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert np.array_equal(op.cpu().numpy().view(np.uint32), ep)
+    assert np.array_equal(ob.cpu().numpy().view(np.uint32), eb)
+    # capacity contract: too-small buffers -> CapacityError with the true count
+    from paper_2601_19911_b200 import CapacityError
+
+    resident.join_build(t(bk), t(br))
+    small = torch.empty(10, dtype=torch.int32, device=cuda)
+    with pytest.raises(CapacityError):
+        resident.join_probe(t(pk), t(pr), small, small.clone())
