@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 offload path (BASELINE.json metric, configs[1] by default).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload join_c2|topk_c1|topk_c3|join_c4]
+    python bench.py --impl reference ...        # the reference's CPU algorithm (oracle port)
+
+One step = one pass of the hot path over one batch of synthetic input:
+  join_*  : hash-join build (all build keys) + probe (this rank's probe keys),
+            emitting (probe row, build row) pairs;
+  topk_*  : Top-K over this rank's keys (+ all-gather/merge when N > 1).
+`value`   = Gkeys/s with inputs resident in HBM (device-timed, CUDA events).
+`e2e`     = the same metric through the public API (B200Device.probe/topk) from
+            pageable host numpy arrays: H2D + kernels + D2H + result objects.
+Rank 0 prints one JSON line. N > 1: launched by torchrun, NCCL, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Top-K/join-probe Gkeys/s (kernel & end-to-end); P95/P99 gated vs always-on vs CPU"
+
+WORKLOADS = {
+    # BASELINE.json configs[1] -- the default N=1 workload
+    "join_c2": dict(kind="join", nb=1_000_000, np=10_000_000, seed=1,
+                    desc="hash-join probe: build 1e6 / probe 1e7 uniform int64 keys in [0, 2e6) as f8, "
+                         "emit (probe rowid, build rowid) pairs"),
+    # BASELINE.json configs[0]
+    "topk_c1": dict(kind="topk", n=1_000_000, k=100, seed=7,
+                    desc="Top-K K=100 over N=1e6 uniform int64 keys in [0, 2^53) as f8 + rowids"),
+    # BASELINE.json configs[2] (one K per run; --k to change)
+    "topk_c3": dict(kind="topk", n=1_000_000_000, k=1000, seed=7,
+                    desc="Top-K over N=1e9 uniform keys per GPU"),
+    # BASELINE.json configs[3], per-GPU probe shard
+    "join_c4": dict(kind="join", nb=100_000_000, np=2_000_000_000, seed=1,
+                    desc="hash-join probe: build 1e8 / probe 2e9 uniform keys in [0, 2e8)"),
+}
+
+
+def _env_int(name: str, default: int) -> int:
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ---- synthetic data ---------------------------------------------------------------
+
+def join_data(wl: dict, rank: int):
+    """Build column (global, identical on every rank) and this rank's probe shard."""
+    nb, np_ = wl["nb"], wl["np"]
+    rng = np.random.Generator(np.random.PCG64(wl["seed"]))
+    bk = rng.integers(0, 2 * nb, size=nb).astype(np.float64)
+    prng = rng if rank == 0 else np.random.Generator(np.random.PCG64([wl["seed"], rank]))
+    pk = prng.integers(0, 2 * nb, size=np_).astype(np.float64)
+    return bk, np.arange(nb, dtype=np.uint32), pk, np.arange(np_, dtype=np.uint32)
+
+
+def topk_data(wl: dict, rank: int):
+    seed = wl["seed"] if rank == 0 else [wl["seed"], rank]
+    rng = np.random.Generator(np.random.PCG64(seed))
+    n = wl["n"]
+    return rng.integers(0, 2**53, size=n, dtype=np.int64).astype(np.float64), np.arange(n, dtype=np.uint32)
+
+
+# ---- clocks (NVML, sampled during the timed region) --------------------------------
+
+_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, device_index: int, period_s: float = 0.01):
+        self.samples: list[tuple[int, int]] = []
+        self.period = period_s
+        self._stop = threading.Event()
+        self._t = None
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = int(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:  # NVML unavailable: report null clocks
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append((int(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)),
+                                     int(get_reasons(self._h))))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        mhz = [s[0] for s in self.samples]
+        bits = 0
+        for _, r in self.samples:
+            bits |= r
+        reasons = [name for b, name in _REASONS.items() if bits & b and name != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(mhz)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---- reference arm / CPU baseline ------------------------------------------------------
+
+def cpu_reference_steps(wl: dict, steps: int, warmup: int, data, threads: int) -> tuple[float, str]:
+    """Times the reference's CPU algorithm (oracle port of ProxyDevice: serial
+    KeyHashTable build + chunk-parallel probe / chunk top-k + merge)."""
+    from oracle import oracle
+
+    oracle.build()
+    times = []
+    if wl["kind"] == "join":
+        bk, br, pk, pr = data
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            t = oracle.Table(bk, br)
+            t.probe(pk, pr, workers=threads)
+            dt = time.perf_counter() - t0
+            if i >= warmup:
+                times.append(dt)
+        units = len(bk) + len(pk)
+        sample = (f"full workload per step: serial build of {len(bk)} + {threads}-thread probe of {len(pk)} "
+                  f"(oracle port of ProxyDevice.probe, device.py:382-436)")
+    else:
+        keys, rows = data
+        k = wl["k"]
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            oracle.proxy_topk(keys, rows, k, threads)
+            dt = time.perf_counter() - t0
+            if i >= warmup:
+                times.append(dt)
+        units = len(keys)
+        sample = (f"full workload per step: {threads}-thread chunk top-{k} + merge over {len(keys)} keys "
+                  f"(oracle port of ProxyDevice.topk, device.py:329-380)")
+    return units / statistics.mean(times) / 1e9, sample
+
+
+def run_reference(args, wl) -> None:
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    data = join_data(wl, 0) if wl["kind"] == "join" else topk_data(wl, 0)
+    # bounded: C2/C1 run in full; the 1e9-scale configs are sampled to 1e8 keys
+    if wl["kind"] == "topk" and wl["n"] > 100_000_000:
+        data = (data[0][:100_000_000], data[1][:100_000_000])
+    if wl["kind"] == "join" and wl["np"] > 100_000_000:
+        data = (data[0][:10_000_000], data[1][:10_000_000], data[2][:100_000_000], data[3][:100_000_000])
+    value, sample = cpu_reference_steps(wl, args.steps, args.warmup, data, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "name": args.workload},
+        "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- B200 arm --------------------------------------------------------------------------
+
+def _peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+def _traffic(workload: str):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        return json.loads(p.read_text()).get(workload)
+    return None
+
+
+def run_b200(args, wl) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_19911_b200 import B200Device, KeyVector, _native, resident, sharded
+
+    rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _native.load()
+    device = B200Device(device=local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    if wl["kind"] == "join":
+        bk, br, pk, pr = join_data(wl, rank)
+        lo, hi = sharded.shard_bounds(len(bk), world, rank)
+        t_bk = torch.from_numpy(bk[lo:hi]).to(dev)
+        t_br = torch.from_numpy(br[lo:hi].view(np.int32)).to(dev)
+        t_pk = torch.from_numpy(pk).to(dev)
+        t_pr = torch.from_numpy(pr.view(np.int32)).to(dev)
+        # size the pair buffers once (first call), then reuse them every step
+        full_bk = torch.cat(sharded._all_gather_ragged(t_bk)) if world > 1 else t_bk
+        full_br = torch.cat(sharded._all_gather_ragged(t_br)) if world > 1 else t_br
+        op0, _ = resident.join(full_bk, full_br, t_pk, t_pr)
+        cap = max(int(op0.numel()), 1)
+        out_p = torch.empty(cap, dtype=torch.int32, device=dev)
+        out_b = torch.empty(cap, dtype=torch.int32, device=dev)
+        del op0, full_bk, full_br
+
+        def step():
+            if world > 1:
+                fbk = torch.cat(sharded._all_gather_ragged(t_bk))
+                fbr = torch.cat(sharded._all_gather_ragged(t_br))
+            else:
+                fbk, fbr = t_bk, t_br
+            resident.join_build(fbk, fbr)
+            return resident.join_probe(t_pk, t_pr, out_p, out_b)
+
+        units = len(bk) + world * len(pk)  # distinct keys joined by the whole job
+        local_units = len(bk) + len(pk)
+    else:
+        keys, rows = topk_data(wl, rank)
+        t_k = torch.from_numpy(keys).to(dev)
+        t_r = torch.from_numpy(rows.view(np.int32)).to(dev)
+        k = wl["k"]
+
+        def step():
+            return sharded.topk(t_k, t_r, k)
+
+        units = world * len(keys)
+        local_units = len(keys)
+
+    # warm-up (also JIT-free: the kernels are precompiled SASS)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    resident.set_profiling(True)
+    kern_ms, build_ms = [], []
+    step_ms = []
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = _native.launch_count()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            m = step()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            kt = _native.kernel_times()
+            if wl["kind"] == "join":
+                kern_ms.append(kt["join_probe_ms"])
+                build_ms.append(kt["join_build_ms"])
+            else:
+                kern_ms.append(kt["topk_filter_ms"])
+    torch.cuda.synchronize()
+    barrier()
+    launches = _native.launch_count() - launches0
+    resident.set_profiling(False)
+    ms = max_over_ranks(statistics.mean(step_ms))
+    value = units / (ms / 1e3) / 1e9
+
+    # roofline of the dominant kernel (per launch, algorithmic bytes)
+    peaks = _peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    kms = statistics.mean(kern_ms)
+    if wl["kind"] == "join":
+        matches = int(m)
+        table_bytes = int(kt["join_capacity"]) * 16
+        l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+        per_probe = 12 + (32 if table_bytes > l2 else 0)
+        alg_bytes = per_probe * len(pk) + 8 * matches
+        kernel = "join_probe_kernel"
+    else:
+        matches = None
+        alg_bytes = 8 * len(keys)
+        kernel = "topk_filter_kernel"
+    achieved = alg_bytes / (kms / 1e3) / 1e9
+
+    # end to end through the public API, pageable host arrays
+    e2e_t = []
+    if wl["kind"] == "join":
+        kv_b, kv_p = KeyVector(bk, br), KeyVector(pk, pr)
+        h2d = 12 * (len(bk) + len(pk))
+        for i in range(args.warmup + args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            res = device.probe(kv_b, kv_p)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                e2e_t.append(dt)
+        d2h = 8 * res.payload.match_count
+        e2e_units = units
+    else:
+        kv = KeyVector(keys, rows)
+        h2d = 12 * len(keys)
+        for i in range(args.warmup + args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            res = device.topk(kv, wl["k"])
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                e2e_t.append(dt)
+        d2h = 4 * len(res.payload.rows)
+        e2e_units = units
+    e2e_s = max_over_ranks(statistics.mean(e2e_t))
+    e2e_value = e2e_units / e2e_s / 1e9
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        data = (bk, br, pk, pr) if wl["kind"] == "join" else (keys, rows)
+        if wl["kind"] == "topk" and wl["n"] > 100_000_000:
+            data = (keys[:100_000_000], rows[:100_000_000])
+        if wl["kind"] == "join" and wl["np"] > 100_000_000:
+            data = (bk[:10_000_000], br[:10_000_000], pk[:100_000_000], pr[:100_000_000])
+        cv, sample = cpu_reference_steps(wl, 3, 1, data, threads)
+        cpu = {"value": cv, "unit": "Gkeys/s", "cores": threads, "kind": "port", "sample": sample}
+
+    device.close()
+    if rank == 0:
+        cfg = {"workload": wl["desc"], "name": args.workload,
+               "l2": "flushed between timed steps (256 MiB write outside the CUDA events)",
+               "units_per_step": units, "local_units_per_step": local_units, "parallelism": f"dp{world}"}
+        if matches is not None:
+            cfg["matches_per_rank"] = matches
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "e2e": {"value": e2e_value, "unit": "Gkeys/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_s * 1e3},
+            "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": _traffic(args.workload),
+                         "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": kms,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "fallback" not in peaks else "fallback"},
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+        }
+        if wl["kind"] == "join":
+            line["roofline"]["build_ms"] = statistics.mean(build_ms)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="join_c2")
+    ap.add_argument("--k", type=int, default=None, help="override K for topk workloads")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    wl = dict(WORKLOADS[args.workload])
+    if args.k is not None:
+        wl["k"] = args.k
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_b200(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -226,12 +226,28 @@ typedef struct {
 
 static void* probe_worker(void* arg) {
   probe_job* j = (probe_job*)arg;
-  const uint64_t n = j->hi - j->lo;
-  j->m = oracle_hash_probe(j->slot_bits, j->slot_rows, j->cap, j->keys + j->lo, j->rows + j->lo, n, NULL, NULL, 0);
-  j->mcap = j->m;
-  j->p = (uint32_t*)malloc((j->m + 1) * 4);
-  j->b = (uint32_t*)malloc((j->m + 1) * 4);
-  oracle_hash_probe(j->slot_bits, j->slot_rows, j->cap, j->keys + j->lo, j->rows + j->lo, n, j->p, j->b, j->mcap);
+  const uint64_t mask = j->cap - 1;
+  uint64_t cap = (j->hi - j->lo) + 16, m = 0;
+  j->p = (uint32_t*)malloc(cap * 4);
+  j->b = (uint32_t*)malloc(cap * 4);
+  for (uint64_t i = j->lo; i < j->hi; ++i) { /* one pass, growable output (host.py:168-188) */
+    const uint64_t b = key_bits(j->keys[i]);
+    uint64_t cur = oracle_mix64(b) & mask;
+    while (j->slot_rows[cur] != ROW_EMPTY) {
+      if (j->slot_bits[cur] == b) {
+        if (m == cap) {
+          cap *= 2;
+          j->p = (uint32_t*)realloc(j->p, cap * 4);
+          j->b = (uint32_t*)realloc(j->b, cap * 4);
+        }
+        j->p[m] = j->rows[i];
+        j->b[m] = j->slot_rows[cur];
+        ++m;
+      }
+      cur = (cur + 1) & mask;
+    }
+  }
+  j->m = m;
   return NULL;
 }
 

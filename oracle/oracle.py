@@ -107,11 +107,14 @@ class Table:
             b = np.empty(m, dtype=np.uint32)
             lib.oracle_hash_probe(*args, _p(p), _p(b), m)
         else:
-            m = lib.oracle_hash_probe(*args, 0, 0, 0)
-            p = np.empty(m, dtype=np.uint32)
-            b = np.empty(m, dtype=np.uint32)
-            got = lib.oracle_proxy_probe(*args, _p(p), _p(b), m, workers)
-            assert got == m
+            cap = max(len(kc), 1)
+            while True:
+                p = np.empty(cap, dtype=np.uint32)
+                b = np.empty(cap, dtype=np.uint32)
+                m = lib.oracle_proxy_probe(*args, _p(p), _p(b), cap, workers)
+                if m <= cap:
+                    return p[:m], b[:m]
+                cap = m
         return p, b
 
 

@@ -92,6 +92,7 @@ struct Ctx {
   bool last_probe_valid = false;
 
   bool prof = false;
+  bool build_timed = false;
   golp_kernel_times kt{};
 };
 
@@ -412,11 +413,15 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   g.jmask = cap - 1;
   g.jnb = nb;
   Slot* table = g.table.as<Slot>();
+  prof_record(4, s);
   join_init_table_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap);
   CKL();
   ++g_launches;
   CK(cudaMemsetAsync(g.jcount.p, 0, 16, s));
-  if (nb == 0) return GOLP_OK;
+  if (nb == 0) {
+    prof_record(5, s);
+    return GOLP_OK;
+  }
   unsigned long long* cursor = g.jcount.as<unsigned long long>();
   unsigned int* big_count = reinterpret_cast<unsigned int*>(cursor + 1);
   const int gb = grid_for(nb, 256, 8);
@@ -441,6 +446,7 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
                                                    g.csr_pos.as<uint32_t>(), brows, g.csr_row.as<uint32_t>());
   CKL();
   g_launches += 5;
+  prof_record(5, s);
   return GOLP_OK;
 }
 
@@ -496,11 +502,14 @@ int join_probe_impl(const double* pkeys, const uint32_t* prows, uint64_t np, uin
   CK(cudaMemsetAsync(g.tile_counter.p, 0, 4, s));
   CK(cudaMemsetAsync(g.totals.p, 0, 16, s));
   unsigned long long* totals = g.totals.as<unsigned long long>();
+  prof_record(6, s);
   if (g.jnb > 0) {
     RET(launch_probe(pkeys, prows, np, out_p, out_b, cap, g.tile_status.as<unsigned long long>(),
                      g.tile_counter.as<unsigned int>(), totals, totals + 1, s));
   }
+  prof_record(7, s);
   RET(read_u64(totals + 1, out_m, s));
+  if (g.prof) g.kt.join_probe_ms = prof_ms(6, 7);
   return GOLP_OK;
 }
 
@@ -572,6 +581,11 @@ int golp_set_profiling(int on) {
 
 int golp_last_kernel_times(golp_kernel_times* out) {
   if (!out) return invalid("null output");
+  if (g.build_timed) {
+    CK(cudaEventSynchronize(g.ev[5]));
+    g.kt.join_build_ms = prof_ms(4, 5);
+    g.build_timed = false;
+  }
   *out = g.kt;
   return GOLP_OK;
 }
@@ -602,14 +616,9 @@ int golp_topk_merge_device(const uint64_t* d_key_codes, const uint32_t* d_rows, 
 int golp_join_build_device(const double* d_build_keys, const uint32_t* d_build_rows, uint64_t nb, void* stream) {
   RET(ensure_init());
   cudaStream_t s = as_stream(stream);
-  prof_record(4, s);
   RET(join_build_impl(d_build_keys, d_build_rows, nb, s));
-  prof_record(5, s);
-  if (g.prof) {
-    CK(cudaStreamSynchronize(s));
-    g.kt.join_build_ms = prof_ms(4, 5);
-    g.kt.join_capacity = g.jcap;
-  }
+  g.build_timed = g.prof;  // resolved lazily by golp_last_kernel_times (no sync here)
+  g.kt.join_capacity = g.jcap;
   return GOLP_OK;
 }
 
@@ -619,13 +628,7 @@ int golp_join_probe_device(const double* d_probe_keys, const uint32_t* d_probe_r
   RET(ensure_init());
   if (!out_matches) return invalid("null out_matches");
   cudaStream_t s = as_stream(stream);
-  prof_record(6, s);
   RET(join_probe_impl(d_probe_keys, d_probe_rows, np, d_out_probe_rows, d_out_build_rows, cap, out_matches, s));
-  prof_record(7, s);
-  if (g.prof) {
-    CK(cudaStreamSynchronize(s));
-    g.kt.join_probe_ms = prof_ms(6, 7);
-  }
   if (*out_matches > cap) {
     set_error("probe output exceeds the supplied capacity");
     return GOLP_ERR_CAPACITY;
