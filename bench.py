@@ -377,7 +377,9 @@ def run_b200(args, wl) -> None:
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
             "e2e": {"value": e2e_value, "unit": "Gkeys/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_s * 1e3},
+                    "ms_per_step": e2e_s * 1e3,
+                    "last_ledger_ms": {f: getattr(res.ledger, f) * 1e3 for f in ("t_h2d", "t_kernel", "t_d2h",
+                                                                                  "t_post")}},
             "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(args.workload),
                          "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": kms,

@@ -84,7 +84,8 @@ struct Ctx {
   cudaEvent_t ev[8] = {};
 
   DevBuf ctl, cand_hi, cand_lo, w_hi, w_lo, out_rows, out_hi, samples;
-  DevBuf table, bslot, brank, csr_pos, csr_row, big_list, jcount, tile_status, tile_counter, totals;
+  DevBuf table, bslot, brank, csr_pos, csr_row, big_list, jcount, wcount, partial, totals, totals2;
+  DevBuf sc_entry, jflags;
   DevBuf pairs_p, pairs_b;
   DevBuf in_keys, in_rows, in_bkeys, in_brows, in_payload;
   uint64_t jcap = 0, jmask = 0, jnb = 0;
@@ -396,8 +397,8 @@ int grid_for(uint64_t n, int threads, int per_sm) {
 
 int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cudaStream_t s) {
   uint64_t cap = 1024;
-  while (cap < 2 * nb) cap <<= 1;
-  if (cap > (1ull << 32)) {
+  while (cap < 2 * nb && cap < (1ull << 32)) cap <<= 1;
+  if (cap < 2 * nb) {
     set_error("join build side too large for 32-bit slot indices");
     return GOLP_ERR_CAPACITY;
   }
@@ -418,6 +419,8 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   CKL();
   ++g_launches;
   CK(cudaMemsetAsync(g.jcount.p, 0, 16, s));
+  CK(g.jflags.ensure(4));
+  CK(cudaMemsetAsync(g.jflags.p, 0, 4, s));
   if (nb == 0) {
     prof_record(5, s);
     return GOLP_OK;
@@ -450,39 +453,49 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   return GOLP_OK;
 }
 
-// One probe launch over [pkeys, pkeys+np); pair offsets continue from *base_in.
+// One probe over [pkeys, pkeys+np): match -> scan of block totals -> emit, per
+// sub-chunk (the sub-chunk bounds the scratch). Pair offsets continue from
+// *base_in; *total_out = *base_in + pairs of this call.
 int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
-                 uint64_t cap, unsigned long long* tile_status, unsigned int* tile_counter,
-                 const unsigned long long* base_in, unsigned long long* total_out, cudaStream_t s) {
-  if (np == 0) {
+                 uint64_t cap, const unsigned long long* base_in, unsigned long long* total_out, cudaStream_t s) {
+  if (np == 0 || g.jnb == 0) {
     CK(cudaMemcpyAsync(total_out, base_in, 8, cudaMemcpyDeviceToDevice, s));
     return GOLP_OK;
   }
-  ProbeArgs a;
-  a.pkeys = pkeys;
-  a.prows = prows;
-  a.np = np;
-  a.table = g.table.as<Slot>();
-  a.mask = g.jmask;
-  a.csr_row = g.csr_row.as<uint32_t>();
-  a.out_p = out_p;
-  a.out_b = out_b;
-  a.cap = cap;
-  a.tile_status = tile_status;
-  a.tile_counter = tile_counter;
-  a.base_in = base_in;
-  a.total_out = total_out;
-  a.ntiles = (np + kProbeTile - 1) / kProbeTile;
-  join_probe_kernel<<<(unsigned)a.ntiles, kProbeThreads, 0, s>>>(a);
-  CKL();
-  ++g_launches;
-  return GOLP_OK;
-}
-
-int ensure_probe_ws(uint64_t ntiles_total, uint64_t launches) {
-  CK(g.tile_status.ensure(std::max<uint64_t>(ntiles_total, 1) * 8));
-  CK(g.tile_counter.ensure(std::max<uint64_t>(launches, 1) * 4));
-  CK(g.totals.ensure((launches + 1) * 8));
+  constexpr uint64_t kSub = 1ull << 27;  // probes per sub-chunk (scratch <= 1 GiB)
+  const uint64_t sub = std::min(np, kSub);
+  const uint64_t nwt_max = (sub + kWarpTile - 1) / kWarpTile;
+  CK(g.sc_entry.ensure(nwt_max * kWarpTile * 8));
+  CK(g.wcount.ensure(nwt_max * 8));
+  CK(g.totals2.ensure(16));
+  MatchScratch sc;
+  sc.entry = g.sc_entry.as<uint2>();
+  sc.nmatch = g.wcount.as<uint32_t>();
+  sc.npairs = sc.nmatch + nwt_max;
+  unsigned long long* tmp = g.totals2.as<unsigned long long>();
+  for (uint64_t c0 = 0; c0 < np; c0 += kSub) {
+    const uint64_t cn = std::min(kSub, np - c0);
+    const uint64_t nwt = (cn + kWarpTile - 1) / kWarpTile;
+    uint64_t blocks = (uint64_t)g.sms * GOLP_PROBE_MINB;
+    blocks = std::max<uint64_t>(blocks, (nwt + kMaxTilesPerBlock - 1) / kMaxTilesPerBlock);
+    blocks = std::min<uint64_t>(blocks, nwt);
+    const uint64_t per_block = (nwt + blocks - 1) / blocks;
+    blocks = (nwt + per_block - 1) / per_block;
+    CK(g.partial.ensure(blocks * 8));
+    unsigned long long* part = g.partial.as<unsigned long long>();
+    join_match_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(pkeys + c0, cn, g.table.as<Slot>(), g.jmask, sc, nwt,
+                                                                 per_block, part, g.jflags.as<unsigned int>());
+    CKL();
+    const bool last = c0 + kSub >= np;
+    const unsigned long long* bin = c0 == 0 ? base_in : tmp + ((c0 / kSub) & 1);
+    unsigned long long* bout = last ? total_out : tmp + (((c0 / kSub) + 1) & 1);
+    scan_partials_kernel<<<1, kScanThreads, 0, s>>>(part, (uint32_t)blocks, bin, bout);
+    CKL();
+    join_emit_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(sc, prows + c0, g.csr_row.as<uint32_t>(), nwt,
+                                                                per_block, part, out_p, out_b, cap);
+    CKL();
+    g_launches += 3;
+  }
   return GOLP_OK;
 }
 
@@ -494,21 +507,30 @@ int read_u64(const void* dptr, uint64_t* out, cudaStream_t s) {
   return GOLP_OK;
 }
 
+// Match count of a finished probe + the kernels' overflow flag (one sync).
+int read_probe_total(const void* dptr, uint64_t* out, cudaStream_t s) {
+  uint64_t* h = static_cast<uint64_t*>(g.pin_small);
+  CK(cudaMemcpyAsync(h, dptr, 8, cudaMemcpyDeviceToHost, s));
+  if (g.jflags.p) CK(cudaMemcpyAsync(h + 1, g.jflags.p, 4, cudaMemcpyDeviceToHost, s));
+  else h[1] = 0;
+  CK(cudaStreamSynchronize(s));
+  *out = h[0];
+  if (g.jflags.p && (uint32_t)h[1] != 0) {
+    set_error("a build key occurs more than 2^24-1 times; the packed probe entry cannot describe it");
+    return GOLP_ERR_CAPACITY;
+  }
+  return GOLP_OK;
+}
+
 int join_probe_impl(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
                     uint64_t cap, uint64_t* out_m, cudaStream_t s) {
-  const uint64_t ntiles = (np + kProbeTile - 1) / kProbeTile;
-  RET(ensure_probe_ws(ntiles, 1));
-  CK(cudaMemsetAsync(g.tile_status.p, 0, std::max<uint64_t>(ntiles, 1) * 8, s));
-  CK(cudaMemsetAsync(g.tile_counter.p, 0, 4, s));
-  CK(cudaMemsetAsync(g.totals.p, 0, 16, s));
+  CK(g.totals.ensure(16));
   unsigned long long* totals = g.totals.as<unsigned long long>();
+  CK(cudaMemsetAsync(totals, 0, 16, s));
   prof_record(6, s);
-  if (g.jnb > 0) {
-    RET(launch_probe(pkeys, prows, np, out_p, out_b, cap, g.tile_status.as<unsigned long long>(),
-                     g.tile_counter.as<unsigned int>(), totals, totals + 1, s));
-  }
+  RET(launch_probe(pkeys, prows, np, out_p, out_b, cap, totals, totals + 1, s));
   prof_record(7, s);
-  RET(read_u64(totals + 1, out_m, s));
+  RET(read_probe_total(totals + 1, out_m, s));
   if (g.prof) g.kt.join_probe_ms = prof_ms(6, 7);
   return GOLP_OK;
 }
@@ -546,7 +568,7 @@ int golp_shutdown(void) {
   g.pool.stop();
   DevBuf* bufs[] = {&g.ctl, &g.cand_hi, &g.cand_lo, &g.w_hi, &g.w_lo, &g.out_rows, &g.out_hi, &g.samples,
                     &g.table, &g.bslot, &g.brank, &g.csr_pos, &g.csr_row, &g.big_list, &g.jcount,
-                    &g.tile_status, &g.tile_counter, &g.totals, &g.pairs_p, &g.pairs_b, &g.in_keys, &g.in_rows,
+                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_entry, &g.jflags, &g.pairs_p, &g.pairs_b, &g.in_keys, &g.in_rows,
                     &g.in_bkeys, &g.in_brows, &g.in_payload};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < kSlots; ++i) {
@@ -769,13 +791,10 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   CK(cudaStreamWaitEvent(s, ev_chunk, 0));
   RET(join_build_impl(dbk, dbr, nb, s));
 
-  uint64_t per_chunk = std::max<uint64_t>(g.chunk / 8, kProbeTile);
-  per_chunk = (per_chunk / kProbeTile) * kProbeTile;
+  uint64_t per_chunk = std::max<uint64_t>(g.chunk / 8, kWarpTile);
+  per_chunk = (per_chunk / kWarpTile) * kWarpTile;
   const uint64_t nchunks = np ? (np + per_chunk - 1) / per_chunk : 0;
-  const uint64_t ntiles_total = (np + kProbeTile - 1) / kProbeTile + nchunks;
-  RET(ensure_probe_ws(ntiles_total, nchunks));
-  CK(cudaMemsetAsync(g.tile_status.p, 0, std::max<uint64_t>(ntiles_total, 1) * 8, s));
-  CK(cudaMemsetAsync(g.tile_counter.p, 0, std::max<uint64_t>(nchunks, 1) * 4, s));
+  CK(g.totals.ensure((nchunks + 1) * 8));
   CK(cudaMemsetAsync(g.totals.p, 0, (nchunks + 1) * 8, s));
   uint64_t out_cap = std::max<uint64_t>(g.pairs_p.bytes / 4, std::max<uint64_t>(np, 1024));
   CK(g.pairs_p.ensure(out_cap * 4));
@@ -783,7 +802,6 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   out_cap = std::min(g.pairs_p.bytes, g.pairs_b.bytes) / 4;
   unsigned long long* totals = g.totals.as<unsigned long long>();
   auto run_chunks = [&](bool with_h2d) -> int {
-    uint64_t tile_off = 0;
     for (uint64_t c = 0; c < nchunks; ++c) {
       const uint64_t c0 = c * per_chunk;
       const uint64_t cn = std::min(per_chunk, np - c0);
@@ -794,14 +812,8 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
         CK(cudaEventRecord(ev_chunk, g.s_h2d));
         CK(cudaStreamWaitEvent(s, ev_chunk, 0));
       }
-      if (g.jnb > 0) {
-        RET(launch_probe(dpk + c0, dpr + c0, cn, g.pairs_p.as<uint32_t>(), g.pairs_b.as<uint32_t>(), out_cap,
-                         g.tile_status.as<unsigned long long>() + tile_off, g.tile_counter.as<unsigned int>() + c,
-                         totals + c, totals + c + 1, s));
-      } else {
-        CK(cudaMemsetAsync(totals + c + 1, 0, 8, s));
-      }
-      tile_off += (cn + kProbeTile - 1) / kProbeTile;
+      RET(launch_probe(dpk + c0, dpr + c0, cn, g.pairs_p.as<uint32_t>(), g.pairs_b.as<uint32_t>(), out_cap,
+                       totals + c, totals + c + 1, s));
     }
     return GOLP_OK;
   };
@@ -812,16 +824,14 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   for (bool& b : g.pin_busy) b = false;
   const double t1 = wall_seconds();
   uint64_t m = 0;
-  RET(read_u64(totals + nchunks, &m, s));
+  RET(read_probe_total(totals + nchunks, &m, s));
   if (m > out_cap) {  // rare: more pairs than probes; grow and re-probe the resident input
     CK(g.pairs_p.ensure(m * 4));
     CK(g.pairs_b.ensure(m * 4));
     out_cap = std::min(g.pairs_p.bytes, g.pairs_b.bytes) / 4;
-    CK(cudaMemsetAsync(g.tile_status.p, 0, std::max<uint64_t>(ntiles_total, 1) * 8, s));
-    CK(cudaMemsetAsync(g.tile_counter.p, 0, std::max<uint64_t>(nchunks, 1) * 4, s));
     CK(cudaMemsetAsync(g.totals.p, 0, (nchunks + 1) * 8, s));
     RET(run_chunks(false));
-    RET(read_u64(totals + nchunks, &m, s));
+    RET(read_probe_total(totals + nchunks, &m, s));
   }
   const double t2 = wall_seconds();
   *out_matches = m;

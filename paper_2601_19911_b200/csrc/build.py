@@ -45,22 +45,25 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > mtime for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    """Compile libgolp_b200.so (or a tuning variant with extra -D defines at `out`)."""
+    target = out or LIB
+    if not force and out is None and not defines and not _stale():
         return LIB
     nvcc = _nvcc()
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc, *ARCH, *FLAGS, "-shared", "-o", str(tmp), *[str(HERE / s) for s in SOURCES], "-lpthread"]
+    tmp = target.with_suffix(".so.tmp")
+    cmd = [nvcc, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", str(tmp),
+           *[str(HERE / s) for s in SOURCES], "-lpthread"]
     proc = subprocess.run(cmd, cwd=HERE, capture_output=True, text=True)
     log = PKG / "build_ptxas.log"
     log.write_text(proc.stdout + proc.stderr)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
         raise RuntimeError(f"nvcc failed ({proc.returncode}); see {log}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, target)
     if verbose:
         sys.stdout.write(proc.stderr)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":

@@ -8,15 +8,17 @@
 //
 // Layout in HBM:
 //   table  : cap x 16 B slots {u64 key_bits, u32 off, u32 cnt}, one slot per
-//            DISTINCT build key, linear probing on mix64(bits) & (cap-1), load <= 0.5.
+//            DISTINCT build key. Linear probing whose start is rounded down to an
+//            even slot: the probe walks 32-byte, sector-aligned slot pairs, one
+//            256-bit load per pair (LDG.E.256). cap = pow2 >= 2*nb (load <= 0.5).
 //   csr_row: nb x u32, the build rows of every key group in build-position order;
 //            groups of one keep their row inline in slot.off (no CSR access).
 // Build: insert (atomicCAS) -> group offsets (warp-aggregated cursor) -> scatter
 // build positions -> per-group sort of positions (thread / block / block-global)
-// -> rows. Probe: one single-pass kernel, 2048 probes per tile: probe the table,
-// block scan of match counts, decoupled look-back for the tile's output offset,
-// emit pairs in probe order.
+// -> rows. Probe: match (one lookup per probe, compacted per warp tile) -> scan
+// -> emit (see below).
 #pragma once
+#include <cooperative_groups.h>
 #include "sortnet.cuh"
 
 namespace golp {
@@ -26,6 +28,12 @@ struct __align__(16) Slot {
   uint32_t off;
   uint32_t cnt;
 };
+
+// First slot of a key's probe sequence: an even slot, so the walk covers whole
+// 32-byte slot pairs.
+__host__ __device__ __forceinline__ uint64_t home_slot(uint64_t bits, uint64_t mask) {
+  return mix64(bits) & mask & ~1ull;
+}
 
 constexpr int kSmallGroup = 32;        // groups up to this size sorted by their leader thread
 constexpr uint32_t kGroupTile = 16384;  // groups up to this size sorted in shared memory (64 KB)
@@ -42,7 +50,7 @@ __global__ void join_insert_kernel(const double* __restrict__ bkeys, uint64_t nb
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += stride) {
     const uint64_t b = canon_bits(__ldg(bkeys + i));
-    uint64_t h = mix64(b) & mask;
+    uint64_t h = home_slot(b, mask);
     while (true) {
       unsigned long long* kp = reinterpret_cast<unsigned long long*>(&table[h].key);
       const unsigned long long k = *(volatile unsigned long long*)kp;
@@ -151,147 +159,284 @@ __global__ void __launch_bounds__(1024) join_big_groups_kernel(const Slot* __res
 }
 
 // ---- probe ------------------------------------------------------------------------
+// Bound by random table lookups: ~1 L1TEX wavefront per lookup, ~0.8/clk/SM
+// from L2 (tools/microbench.cu, tools/probe_ladder.cu). Every probe key is looked
+// up exactly once:
+//   match : each block walks a contiguous range of warp tiles (32*kWarpItems
+//           consecutive probes); a warp resolves its probes (linear probing over
+//           32-byte slot pairs) and
+//           compacts the hits, in probe order, into the tile's scratch segment as
+//           8-byte entries {slot.off, slot.cnt << 8 | position in tile};
+//           per-tile entry / pair counts and the block's pair total are written.
+//   scan  : one block scans the per-block totals (+ pairs of earlier launches).
+//   emit  : same block -> tile-range mapping; a block scan of the tiles' pair
+//           counts gives each tile's output offset; warps expand entries to
+//           (probe row, build row) pairs.
+// Output order = probe position, then CSR (build insertion) order.
+#ifndef GOLP_WARP_ITEMS
+#define GOLP_WARP_ITEMS 2
+#endif
+#ifndef GOLP_PROBE_MINB
+#define GOLP_PROBE_MINB 6
+#endif
+constexpr int kWarpItems = GOLP_WARP_ITEMS;
+constexpr uint32_t kWarpTile = 32 * kWarpItems;  // probes per warp tile
+static_assert(kWarpTile <= 256, "entry position is 8 bits");
 constexpr int kProbeThreads = 256;
-constexpr int kProbeItems = 8;
-constexpr uint32_t kProbeTile = kProbeThreads * kProbeItems;  // 2048 probes
-constexpr unsigned long long kFlagA = 1ull << 62;  // tile aggregate published
-constexpr unsigned long long kFlagP = 2ull << 62;  // inclusive prefix published
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
+constexpr uint32_t kMaxTilesPerBlock = 4096;
+constexpr uint32_t kMaxGroup = (1u << 24) - 1;  // largest key group an entry can describe
 
-struct ProbeArgs {
-  const double* pkeys;
-  const uint32_t* prows;
-  uint64_t np;
-  const Slot* table;
-  uint64_t mask;
-  const uint32_t* csr_row;
-  uint32_t* out_p;
-  uint32_t* out_b;
-  uint64_t cap;
-  unsigned long long* tile_status;  // ntiles entries, zeroed
-  unsigned int* tile_counter;       // zeroed
-  const unsigned long long* base_in;  // pairs emitted before this launch
-  unsigned long long* total_out;      // base_in + pairs of this launch
-  uint64_t ntiles;
-};
+// L2 eviction policies: the table should survive the probe stream in L2, the
+// streamed probe columns should not displace it.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
-__device__ __forceinline__ ulonglong2 ldg_slot(const Slot* s) {
-  ulonglong2 r;
-  asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(s));
+// Both slots of a 32-byte aligned pair in one 256-bit load (LDG.E.ENL2.256).
+__device__ __forceinline__ ulonglong4 ldg_pair(const Slot* s, uint64_t pol) {
+  ulonglong4 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+               : "=l"(r.x), "=l"(r.y), "=l"(r.z), "=l"(r.w)
+               : "l"(s), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double2 ldg_stream_d2(const double* p, uint64_t pol) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint4 ldg_stream_u4(const uint32_t* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
   return r;
 }
 
-__global__ void __launch_bounds__(kProbeThreads) join_probe_kernel(ProbeArgs a) {
-  __shared__ unsigned s_tile;
-  __shared__ unsigned long long s_warp[kProbeThreads / 32];
-  __shared__ unsigned long long s_base;
-  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
-  __syncthreads();
-  const uint64_t tile = s_tile;
-  const uint64_t first = tile * kProbeTile + (uint64_t)threadIdx.x * kProbeItems;
+// ---- block scan helpers ----------------------------------------------------------
+constexpr int kScanThreads = 1024;
 
-  double k[kProbeItems];
-  const bool full = first + kProbeItems <= a.np && (((uintptr_t)(a.pkeys + first) & 15) == 0);
-  if (full) {
-#pragma unroll
-    for (int j = 0; j < kProbeItems; j += 2) {
-      const double2 v = ldg_nc_d2(a.pkeys + first + j);
-      k[j] = v.x;
-      k[j + 1] = v.y;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < kProbeItems; ++j) k[j] = (first + j < a.np) ? a.pkeys[first + j] : 0.0;
-  }
-  uint64_t bits[kProbeItems];
-  uint64_t h[kProbeItems];
-  ulonglong2 s[kProbeItems];
-#pragma unroll
-  for (int j = 0; j < kProbeItems; ++j) {
-    bits[j] = canon_bits(k[j]);
-    h[j] = mix64(bits[j]) & a.mask;
-  }
-#pragma unroll
-  for (int j = 0; j < kProbeItems; ++j) s[j] = ldg_slot(a.table + h[j]);
-  uint32_t off[kProbeItems], cnt[kProbeItems];
-  unsigned long long total = 0;
-#pragma unroll
-  for (int j = 0; j < kProbeItems; ++j) {
-    cnt[j] = 0;
-    off[j] = 0;
-    if (first + j < a.np) {
-      ulonglong2 sl = s[j];
-      uint64_t hh = h[j];
-      while (sl.x != bits[j] && sl.x != kEmptyKey) {
-        hh = (hh + 1) & a.mask;
-        sl = ldg_slot(a.table + hh);
-      }
-      if (sl.x == bits[j]) {
-        off[j] = (uint32_t)sl.y;
-        cnt[j] = (uint32_t)(sl.y >> 32);
-      }
-    }
-    total += cnt[j];
-  }
-
-  // block-wide exclusive scan of per-thread match totals
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* s_w,
+                                                              unsigned long long* total) {
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  unsigned long long incl = total;
+  unsigned long long incl = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if ((int)lane >= o) incl += v;
+    const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if ((int)lane >= o) incl += u;
   }
-  if (lane == 31) s_warp[warp] = incl;
+  if (lane == 31) s_w[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    unsigned long long w = lane < kProbeThreads / 32 ? s_warp[lane] : 0ull;
+    const unsigned long long w = lane < (blockDim.x >> 5) ? s_w[lane] : 0ull;
     unsigned long long wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, wi, o);
-      if ((int)lane >= o) wi += v;
+      const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if ((int)lane >= o) wi += u;
     }
-    if (lane < kProbeThreads / 32) s_warp[lane] = wi - w;  // exclusive warp offsets
-    const unsigned long long tile_total = __shfl_sync(0xFFFFFFFFu, wi, kProbeThreads / 32 - 1);
-    if (lane == 0) {
-      // decoupled look-back (single-pass prefix scan over tiles)
-      volatile unsigned long long* st = a.tile_status;
-      unsigned long long excl;
-      if (tile == 0) {
-        excl = *a.base_in;
-        st[0] = kFlagP | ((excl + tile_total) & kValMask);
-      } else {
-        st[tile] = kFlagA | (tile_total & kValMask);
-        excl = 0;
-        int64_t pred = (int64_t)tile - 1;
-        while (true) {
-          const unsigned long long v = st[pred];
-          if ((v >> 62) == 0) continue;  // not yet published
-          excl += v & kValMask;
-          if ((v >> 62) == 2) break;
-          --pred;
-        }
-        __threadfence();
-        st[tile] = kFlagP | ((excl + tile_total) & kValMask);
-      }
-      if (tile == a.ntiles - 1) *a.total_out = excl + tile_total;
-      s_base = excl;
-    }
+    if (lane < (blockDim.x >> 5)) s_w[lane] = wi - w;
+    if (lane == 31) s_w[32] = wi;
   }
   __syncthreads();
-  unsigned long long o = s_base + s_warp[warp] + (incl - total);
+  const unsigned long long r = s_w[warp] + incl - v;
+  *total = s_w[32];
+  __syncthreads();
+  return r;
+}
+
+// One block: exclusive scan of the partials, offset by *base_in; writes *total_out.
+__global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(unsigned long long* partial, uint32_t nparts,
+                                                                     const unsigned long long* base_in,
+                                                                     unsigned long long* total_out) {
+  __shared__ unsigned long long s_w[33];
+  unsigned long long carry = *base_in;
+  for (uint32_t b0 = 0; b0 < nparts; b0 += blockDim.x) {
+    const uint32_t i = b0 + threadIdx.x;
+    const unsigned long long v = i < nparts ? partial[i] : 0ull;
+    unsigned long long tot;
+    const unsigned long long e = block_excl_scan(v, s_w, &tot);
+    if (i < nparts) partial[i] = carry + e;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *total_out = carry;
+}
+
+__device__ __forceinline__ void st_hint(uint32_t* p, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+
+// Checks one slot pair: 1 = found (off/cnt set), 0 = absent, -1 = continue at h+2.
+__device__ __forceinline__ int check_pair(const ulonglong4& sl, uint64_t bits, uint32_t& off, uint32_t& cnt) {
+  if (sl.x == bits) { off = (uint32_t)sl.y; cnt = (uint32_t)(sl.y >> 32); return 1; }
+  if (sl.x == kEmptyKey) return 0;
+  if (sl.z == bits) { off = (uint32_t)sl.w; cnt = (uint32_t)(sl.w >> 32); return 1; }
+  if (sl.z == kEmptyKey) return 0;
+  return -1;
+}
+
+struct MatchScratch {
+  uint2* entry;      // kWarpTile per warp tile: {slot.off, cnt << 8 | pos}
+  uint32_t* nmatch;  // per warp tile
+  uint32_t* npairs;  // per warp tile
+};
+
+__global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_kernel(
+    const double* __restrict__ pkeys, uint64_t np, const Slot* __restrict__ table, uint64_t mask, MatchScratch sc,
+    uint64_t nwt, uint64_t per_block, unsigned long long* __restrict__ bpart, unsigned int* __restrict__ flags) {
+  __shared__ unsigned long long s_w[kProbeThreads / 32];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  constexpr unsigned kWarps = kProbeThreads / 32;
+  const uint64_t pol_stream = policy_evict_first(), pol_table = policy_evict_last();
+  const uint64_t lo = blockIdx.x * per_block, hi = lo + per_block < nwt ? lo + per_block : nwt;
+  const uint32_t pm = (uint32_t)mask;
+  unsigned long long mine = 0;
+  for (uint64_t wt = lo + warp; wt < hi; wt += kWarps) {
+    const uint64_t first = wt * kWarpTile + lane * kWarpItems;
+    double k[kWarpItems];
+    if (first + kWarpItems <= np && (((uintptr_t)(pkeys + first) & 15) == 0)) {
 #pragma unroll
-  for (int j = 0; j < kProbeItems; ++j) {
-    if (cnt[j] == 0) continue;
-    const uint32_t pr = __ldg(a.prows + first + j);
-    if (cnt[j] == 1) {
-      if (o < a.cap) { a.out_p[o] = pr; a.out_b[o] = off[j]; }
-      ++o;
-    } else {
-      for (uint32_t m = 0; m < cnt[j]; ++m, ++o) {
-        if (o < a.cap) { a.out_p[o] = pr; a.out_b[o] = __ldg(a.csr_row + off[j] + m); }
+      for (int j = 0; j < kWarpItems; j += 2) {
+        const double2 v = ldg_stream_d2(pkeys + first + j, pol_stream);
+        k[j] = v.x;
+        k[j + 1] = v.y;
       }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kWarpItems; ++j) k[j] = first + j < np ? pkeys[first + j] : 0.0;
+    }
+    uint64_t bits[kWarpItems];
+    uint32_t h[kWarpItems], off[kWarpItems], cnt[kWarpItems];
+    unsigned pending = 0;
+#pragma unroll
+    for (int j = 0; j < kWarpItems; ++j) {
+      bits[j] = canon_bits(k[j]);
+      h[j] = (uint32_t)home_slot(bits[j], mask);
+      off[j] = 0;
+      cnt[j] = 0;
+      if (first + j < np) pending |= 1u << j;
+    }
+    while (pending) {
+      ulonglong4 sl[kWarpItems];
+#pragma unroll
+      for (int j = 0; j < kWarpItems; ++j)
+        if (pending & (1u << j)) sl[j] = ldg_pair(table + h[j], pol_table);
+#pragma unroll
+      for (int j = 0; j < kWarpItems; ++j) {
+        if (!(pending & (1u << j))) continue;
+        const int st = check_pair(sl[j], bits[j], off[j], cnt[j]);
+        if (st >= 0) pending &= ~(1u << j);
+        else h[j] = (h[j] + 2) & pm;
+      }
+    }
+    uint32_t nm = 0, npr = 0;
+#pragma unroll
+    for (int j = 0; j < kWarpItems; ++j) {
+      nm += cnt[j] != 0;
+      npr += cnt[j];
+    }
+    uint32_t incl = nm;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if ((int)lane >= o) incl += v;
+    }
+    uint32_t pairs = npr;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xFFFFFFFFu, pairs, o);
+    mine += pairs;
+    if (lane == 31) {
+      sc.nmatch[wt] = incl;
+      sc.npairs[wt] = pairs;
+    }
+    uint64_t o = wt * kWarpTile + (incl - nm);
+#pragma unroll
+    for (int j = 0; j < kWarpItems; ++j) {
+      if (cnt[j]) {
+        if (cnt[j] > kMaxGroup) atomicOr(flags, 1u);  // host re-runs without the packed entry
+        sc.entry[o++] = make_uint2(off[j], (cnt[j] << 8) | (lane * kWarpItems + j));
+      }
+    }
+  }
+  if (lane == 0) s_w[warp] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (unsigned w = 0; w < kWarps; ++w) t += s_w[w];
+    bpart[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch sc, const uint32_t* __restrict__ prows,
+                                                                  const uint32_t* __restrict__ csr_row, uint64_t nwt,
+                                                                  uint64_t per_block,
+                                                                  const unsigned long long* __restrict__ bpart,
+                                                                  uint32_t* __restrict__ out_p,
+                                                                  uint32_t* __restrict__ out_b, uint64_t cap) {
+  __shared__ unsigned long long s_off[kMaxTilesPerBlock];
+  __shared__ unsigned long long s_w[33];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  constexpr unsigned kWarps = kProbeThreads / 32;
+  const uint64_t lo = blockIdx.x * per_block, hi = lo + per_block < nwt ? lo + per_block : nwt;
+  if (lo >= hi) return;
+  const uint32_t n = (uint32_t)(hi - lo);
+  unsigned long long carry = bpart[blockIdx.x];
+  for (uint32_t b0 = 0; b0 < n; b0 += kProbeThreads) {
+    const uint32_t i = b0 + threadIdx.x;
+    const unsigned long long v = i < n ? sc.npairs[lo + i] : 0ull;
+    unsigned long long t;
+    const unsigned long long e = block_excl_scan(v, s_w, &t);
+    if (i < n) s_off[i] = carry + e;
+    carry += t;
+  }
+  __syncthreads();
+  const uint64_t pol_stream = policy_evict_first();
+  for (uint64_t t = lo + warp; t < hi; t += kWarps) {
+    const uint32_t nm = sc.nmatch[t];
+    if (nm == 0) continue;
+    unsigned long long run = s_off[t - lo];
+    const uint64_t e0 = t * kWarpTile;
+    for (uint32_t i0 = 0; i0 < nm; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      uint32_t c = 0, pr = 0, of = 0;
+      if (i < nm) {
+        const uint2 en = __ldcs(sc.entry + e0 + i);
+        of = en.x;
+        c = en.y >> 8;
+        pr = __ldg(prows + e0 + (en.y & 255u));
+      }
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((int)lane >= o) incl += v;
+      }
+      const uint32_t gtot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      // singletons (slot.off is the build row) land at consecutive positions;
+      // the rare multi-match entries expand their CSR run serially
+      unsigned long long g = run + (incl - c);
+      if (c == 1) {
+        if (g < cap) {
+          st_hint(out_p + g, pr, pol_stream);
+          st_hint(out_b + g, of, pol_stream);
+        }
+      } else {
+        for (uint32_t m = 0; m < c; ++m, ++g)
+          if (g < cap) {
+            st_hint(out_p + g, pr, pol_stream);
+            st_hint(out_b + g, __ldg(csr_row + of + m), pol_stream);
+          }
+      }
+      run += gtot;
     }
   }
 }

@@ -1,0 +1,315 @@
+// Incremental probe microbenchmarks on a realistic C2 table (1e6 build keys in
+// [0, 2e6), 2^21 slots, 16-B slots in 32-B pairs), 1e7 probe keys. Each rung adds
+// one ingredient of join_probe_coop_kernel; the jump between rungs locates the cost.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/probe_ladder tools/probe_ladder.cu
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull; z ^= z >> 27; z *= 0x94D049BB133111EBull; z ^= z >> 31; return z;
+}
+constexpr uint64_t kEmpty = ~0ull;
+
+__device__ __forceinline__ ulonglong4 ldg_pair(const ulonglong2* s) {
+  ulonglong4 r;
+  asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(r.x), "=l"(r.y), "=l"(r.z), "=l"(r.w) : "l"(s));
+  return r;
+}
+
+// rung 1: hash of index only (pure random-lookup throughput, 1 round)
+template <int W>
+__global__ void r1(const ulonglong2* t, uint64_t mask, uint64_t n, unsigned long long* out) {
+  unsigned long long acc = 0;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = tid * W; i < n; i += st * W) {
+    ulonglong4 v[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) v[j] = ldg_pair(t + ((mix64(i + j) & mask) & ~1ull));
+#pragma unroll
+    for (int j = 0; j < W; ++j) acc += v[j].x == 5;
+  }
+  if (acc == 0x123456) *out = acc;
+}
+
+// rung 2: keys streamed from memory (blocked, W per thread), 1 round, count hits
+template <int W>
+__global__ void r2(const double* keys, const ulonglong2* t, uint64_t mask, uint64_t n, unsigned long long* out) {
+  unsigned long long acc = 0;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = tid * W; i < n; i += st * W) {
+    uint64_t b[W];
+    ulonglong4 v[W];
+#pragma unroll
+    for (int j = 0; j < W; j += 2) {
+      double2 k = __ldg(reinterpret_cast<const double2*>(keys + i + j));
+      b[j] = __double_as_longlong(k.x); b[j + 1] = __double_as_longlong(k.y);
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) v[j] = ldg_pair(t + ((mix64(b[j]) & mask) & ~1ull));
+#pragma unroll
+    for (int j = 0; j < W; ++j) acc += (v[j].x == b[j]) | (v[j].z == b[j]);
+  }
+  if (acc == 0x123456) *out = acc;
+}
+
+// rung 3: full linear-probing resolution (rounds until hit/empty), count hits
+template <int W>
+__global__ void r3(const double* keys, const ulonglong2* t, uint64_t mask, uint64_t n, unsigned long long* out) {
+  unsigned long long acc = 0;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = tid * W; i < n; i += st * W) {
+    uint64_t b[W];
+    uint32_t h[W];
+#pragma unroll
+    for (int j = 0; j < W; j += 2) {
+      double2 k = __ldg(reinterpret_cast<const double2*>(keys + i + j));
+      b[j] = __double_as_longlong(k.x); b[j + 1] = __double_as_longlong(k.y);
+    }
+    unsigned pend = (1u << W) - 1;
+#pragma unroll
+    for (int j = 0; j < W; ++j) h[j] = (uint32_t)((mix64(b[j]) & mask) & ~1ull);
+    while (pend) {
+      ulonglong4 v[W];
+#pragma unroll
+      for (int j = 0; j < W; ++j) if (pend >> j & 1) v[j] = ldg_pair(t + h[j]);
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        if (!(pend >> j & 1)) continue;
+        if (v[j].x == b[j] || v[j].z == b[j]) { acc += 1; pend &= ~(1u << j); }
+        else if (v[j].x == kEmpty || v[j].z == kEmpty) pend &= ~(1u << j);
+        else h[j] = (h[j] + 2) & (uint32_t)mask;
+      }
+    }
+  }
+  if (acc == 0x123456) *out = acc;
+}
+
+// rung 4: rung 3 + per-lane scratch stores of hits (3 x u32) at warp-compacted positions
+template <int W>
+__global__ void r4(const double* keys, const uint32_t* rows, const ulonglong2* t, uint64_t mask, uint64_t n,
+                   uint32_t* sp, uint32_t* so, uint32_t* sc, uint32_t* wcnt) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
+  const unsigned lane = threadIdx.x & 31;
+  for (uint64_t i0 = (tid - lane) * W; i0 < n; i0 += st * W) {
+    const uint64_t i = i0 + lane * W;
+    uint64_t b[W];
+    uint32_t h[W], off[W], cnt[W];
+#pragma unroll
+    for (int j = 0; j < W; j += 2) {
+      double2 k = __ldg(reinterpret_cast<const double2*>(keys + i + j));
+      b[j] = __double_as_longlong(k.x); b[j + 1] = __double_as_longlong(k.y);
+    }
+    unsigned pend = (1u << W) - 1;
+#pragma unroll
+    for (int j = 0; j < W; ++j) { h[j] = (uint32_t)((mix64(b[j]) & mask) & ~1ull); off[j] = cnt[j] = 0; }
+    while (pend) {
+      ulonglong4 v[W];
+#pragma unroll
+      for (int j = 0; j < W; ++j) if (pend >> j & 1) v[j] = ldg_pair(t + h[j]);
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        if (!(pend >> j & 1)) continue;
+        if (v[j].x == b[j]) { off[j] = (uint32_t)v[j].y; cnt[j] = (uint32_t)(v[j].y >> 32); pend &= ~(1u << j); }
+        else if (v[j].x == kEmpty) pend &= ~(1u << j);
+        else if (v[j].z == b[j]) { off[j] = (uint32_t)v[j].w; cnt[j] = (uint32_t)(v[j].w >> 32); pend &= ~(1u << j); }
+        else if (v[j].z == kEmpty) pend &= ~(1u << j);
+        else h[j] = (h[j] + 2) & (uint32_t)mask;
+      }
+    }
+    uint32_t nm = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) nm += cnt[j] != 0;
+    uint32_t incl = nm;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { uint32_t v = __shfl_up_sync(~0u, incl, o); if ((int)lane >= o) incl += v; }
+    if (lane == 31) wcnt[i0 / (32 * W)] = incl;
+    uint4 r = __ldg(reinterpret_cast<const uint4*>(rows + i));
+    uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+    uint64_t o = i0 + (incl - nm);
+#pragma unroll
+    for (int j = 0; j < W; ++j) if (cnt[j]) { sp[o] = rr[j & 3]; so[o] = off[j]; sc[o] = cnt[j]; ++o; }
+  }
+}
+
+
+// rung 5: one round per item; unresolved items go to a block queue in smem,
+// resolved by the whole block after the grid-stride loop (count hits)
+template <int W>
+__global__ void r5(const double* keys, const ulonglong2* t, uint64_t mask, uint64_t n, unsigned long long* out,
+                   ulonglong2* gq) {
+  __shared__ unsigned qn;
+  if (threadIdx.x == 0) qn = 0;
+  __syncthreads();
+  ulonglong2* q = gq + (uint64_t)blockIdx.x * 65536;
+  unsigned long long acc = 0;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = tid * W; i < n; i += st * W) {
+    uint64_t b[W];
+    ulonglong4 v[W];
+#pragma unroll
+    for (int j = 0; j < W; j += 2) {
+      double2 k = __ldg(reinterpret_cast<const double2*>(keys + i + j));
+      b[j] = __double_as_longlong(k.x); b[j + 1] = __double_as_longlong(k.y);
+    }
+    uint32_t h[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) { h[j] = (uint32_t)((mix64(b[j]) & mask) & ~1ull); v[j] = ldg_pair(t + h[j]); }
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      if (v[j].x == b[j] || v[j].z == b[j]) acc += 1;
+      else if (v[j].x != kEmpty && v[j].z != kEmpty) {
+        unsigned p = atomicAdd(&qn, 1u);
+        if (p < 65536) q[p] = make_ulonglong2(b[j], (h[j] + 2) & (uint32_t)mask);
+      }
+    }
+  }
+  __syncthreads();
+  const unsigned m = qn < 65536 ? qn : 65536;
+  for (unsigned k = threadIdx.x; k < m; k += blockDim.x) {
+    ulonglong2 it = q[k];
+    uint32_t h = (uint32_t)it.y;
+    while (true) {
+      ulonglong4 v = ldg_pair(t + h);
+      if (v.x == it.x || v.z == it.x) { acc += 1; break; }
+      if (v.x == kEmpty || v.z == kEmpty) break;
+      h = (h + 2) & (uint32_t)mask;
+    }
+  }
+  if (acc == 0x123456) *out = acc;
+}
+
+// rung 6: rung 3 + hits compacted per warp through shared memory, then
+// coalesced stores of (prow, off, cnt) + per-warp-tile count
+template <int W>
+__global__ void r6(const double* keys, const uint32_t* rows, const ulonglong2* t, uint64_t mask, uint64_t n,
+                   uint32_t* sp, uint32_t* so, uint32_t* sc, uint32_t* wcnt) {
+  __shared__ uint32_t stg[8][3][32 * W];
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t i0 = (tid - lane) * W; i0 < n; i0 += st * W) {
+    const uint64_t i = i0 + lane * W;
+    uint64_t b[W];
+    uint32_t h[W], off[W], cnt[W];
+#pragma unroll
+    for (int j = 0; j < W; j += 2) {
+      double2 k = __ldg(reinterpret_cast<const double2*>(keys + i + j));
+      b[j] = __double_as_longlong(k.x); b[j + 1] = __double_as_longlong(k.y);
+    }
+    unsigned pend = (1u << W) - 1;
+#pragma unroll
+    for (int j = 0; j < W; ++j) { h[j] = (uint32_t)((mix64(b[j]) & mask) & ~1ull); off[j] = cnt[j] = 0; }
+    while (pend) {
+      ulonglong4 v[W];
+#pragma unroll
+      for (int j = 0; j < W; ++j) if (pend >> j & 1) v[j] = ldg_pair(t + h[j]);
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        if (!(pend >> j & 1)) continue;
+        if (v[j].x == b[j]) { off[j] = (uint32_t)v[j].y; cnt[j] = (uint32_t)(v[j].y >> 32); pend &= ~(1u << j); }
+        else if (v[j].x == kEmpty) pend &= ~(1u << j);
+        else if (v[j].z == b[j]) { off[j] = (uint32_t)v[j].w; cnt[j] = (uint32_t)(v[j].w >> 32); pend &= ~(1u << j); }
+        else if (v[j].z == kEmpty) pend &= ~(1u << j);
+        else h[j] = (h[j] + 2) & (uint32_t)mask;
+      }
+    }
+    uint32_t nm = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) nm += cnt[j] != 0;
+    uint32_t incl = nm;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { uint32_t v = __shfl_up_sync(~0u, incl, o); if ((int)lane >= o) incl += v; }
+    const uint32_t tot = __shfl_sync(~0u, incl, 31);
+    if (lane == 31) wcnt[i0 / (32 * W)] = incl;
+    uint4 r = __ldg(reinterpret_cast<const uint4*>(rows + i));
+    uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+    uint32_t o = incl - nm;
+#pragma unroll
+    for (int j = 0; j < W; ++j) if (cnt[j]) { stg[warp][0][o] = rr[j & 3]; stg[warp][1][o] = off[j]; stg[warp][2][o] = cnt[j]; ++o; }
+    __syncwarp();
+    for (uint32_t e = lane; e < tot; e += 32) { sp[i0 + e] = stg[warp][0][e]; so[i0 + e] = stg[warp][1][e]; sc[i0 + e] = stg[warp][2][e]; }
+    __syncwarp();
+  }
+}
+
+int main() {
+  const uint64_t nb = 1000000, np = 10000000, cap = 1 << 21, mask = cap - 1;
+  std::mt19937_64 rng(1);
+  std::vector<double> bk(nb), pk(np);
+  for (auto& x : bk) x = (double)(rng() % (2 * nb));
+  for (auto& x : pk) x = (double)(rng() % (2 * nb));
+  std::vector<ulonglong2> tab(cap, ulonglong2{kEmpty, 0});
+  uint64_t uniq = 0;
+  for (double k : bk) {
+    uint64_t b; memcpy(&b, &k, 8);
+    uint64_t h = (mix64(b) & mask) & ~1ull;
+    while (tab[h].x != kEmpty && tab[h].x != b) h = (h + 1) & mask;
+    if (tab[h].x == kEmpty) { tab[h].x = b; tab[h].y = (1ull << 32) | (uint32_t)uniq; ++uniq; }
+  }
+  printf("unique %llu load %.3f\n", (unsigned long long)uniq, (double)uniq / cap);
+  int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  ulonglong2* dt; double* dk; uint32_t *dr, *sp, *so, *sc, *wc; unsigned long long* out;
+  CK(cudaMalloc(&dt, cap * 16)); CK(cudaMalloc(&dk, np * 8)); CK(cudaMalloc(&dr, np * 4));
+  CK(cudaMalloc(&sp, np * 4)); CK(cudaMalloc(&so, np * 4)); CK(cudaMalloc(&sc, np * 4)); CK(cudaMalloc(&wc, np / 32 * 4 + 64));
+  CK(cudaMalloc(&out, 8));
+  CK(cudaMemcpy(dt, tab.data(), cap * 16, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dk, pk.data(), np * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemset(dr, 1, np * 4));
+  void* flush; CK(cudaMalloc(&flush, 256 << 20));
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  auto run = [&](const char* name, auto fn) {
+    float best = 1e9, tot = 0;
+    for (int r = 0; r < 7; ++r) {
+      cudaMemset(flush, r, 256 << 20);
+      ulonglong2* tmp; (void)tmp;
+      // re-warm the table like the build would
+      cudaMemcpy(dt, dt, 0, cudaMemcpyDeviceToDevice);
+      cudaEventRecord(a); fn(); cudaEventRecord(b); cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b); best = ms < best ? ms : best; tot += ms;
+    }
+    printf("%-48s best %7.1f us  (%s)\n", name, best * 1e3, cudaGetErrorString(cudaGetLastError()));
+  };
+  ulonglong2* gq; CK(cudaMalloc(&gq, (uint64_t)sms * 8 * 65536 * 16));
+  for (int bpsm : {4, 8}) {
+    char nm[96];
+    const int grid = sms * bpsm;
+    snprintf(nm, 96, "r1 idx-hash 1 round W4   grid %dx256", grid);
+    run(nm, [&] { r1<4><<<grid, 256>>>(dt, mask, np, out); });
+    snprintf(nm, 96, "r2 keys + 1 round W4     grid %dx256", grid);
+    run(nm, [&] { r2<4><<<grid, 256>>>(dk, dt, mask, np, out); });
+    snprintf(nm, 96, "r3 keys + full probe W4  grid %dx256", grid);
+    run(nm, [&] { r3<4><<<grid, 256>>>(dk, dt, mask, np, out); });
+    snprintf(nm, 96, "r5 keys + deferred queue W4 grid %dx256", grid);
+    run(nm, [&] { r5<4><<<grid, 256>>>(dk, dt, mask, np, out, gq); });
+    snprintf(nm, 96, "r4 + scratch stores W4   grid %dx256", grid);
+    run(nm, [&] { r4<4><<<grid, 256>>>(dk, dr, dt, mask, np, sp, so, sc, wc); });
+    snprintf(nm, 96, "r6 + smem-staged stores W4 grid %dx256", grid);
+    run(nm, [&] { r6<4><<<grid, 256>>>(dk, dr, dt, mask, np, sp, so, sc, wc); });
+  }
+  // lower load factors (same keys, bigger tables)
+  for (uint64_t c2 : {uint64_t(1) << 22, uint64_t(1) << 23}) {
+    const uint64_t m2 = c2 - 1;
+    std::vector<ulonglong2> t2(c2, ulonglong2{kEmpty, 0});
+    for (double k : bk) {
+      uint64_t b; memcpy(&b, &k, 8);
+      uint64_t h = (mix64(b) & m2) & ~1ull;
+      while (t2[h].x != kEmpty && t2[h].x != b) h = (h + 1) & m2;
+      if (t2[h].x == kEmpty) { t2[h].x = b; t2[h].y = (1ull << 32); }
+    }
+    ulonglong2* d2; CK(cudaMalloc(&d2, c2 * 16));
+    CK(cudaMemcpy(d2, t2.data(), c2 * 16, cudaMemcpyHostToDevice));
+    char nm[96];
+    snprintf(nm, 96, "r3 full probe W4 cap 2^%d (load %.3f)", (int)__builtin_ctzll(c2), (double)uniq / c2);
+    run(nm, [&] { r3<4><<<sms * 8, 256>>>(dk, d2, m2, np, out); });
+    snprintf(nm, 96, "r6 staged stores W4 cap 2^%d", (int)__builtin_ctzll(c2));
+    run(nm, [&] { r6<4><<<sms * 8, 256>>>(dk, dr, d2, m2, np, sp, so, sc, wc); });
+    cudaFree(d2);
+  }
+  return 0;
+}
