@@ -325,34 +325,39 @@ def run_b200(args, wl) -> None:
         kernel = "topk_filter_kernel"
     achieved = alg_bytes / (kms / 1e3) / 1e9
 
-    # end to end through the public API, pageable host arrays
-    e2e_t = []
+    # end to end through the public API from host numpy arrays. Default device:
+    # reused input columns get page-locked after their 2nd use (PinCache), results
+    # land in the pinned arena; a second device with pinning off gives the
+    # staged (pageable-copy) number for the same calls.
+    big = units > 200_000_000  # 1e9-scale workloads: bounded E2E sample (12 GB per call)
+    e2e_steps, e2e_warm = (min(args.steps, 2), 2) if big else (args.steps, args.warmup)
+
+    def e2e_run(dev_):
+        ts = []
+        res_ = None
+        for i in range(e2e_warm + e2e_steps):
+            barrier()
+            t0 = time.perf_counter()
+            res_ = dev_.probe(kv_b, kv_p) if wl["kind"] == "join" else dev_.topk(kv, wl["k"])
+            dt = time.perf_counter() - t0
+            if i >= e2e_warm:
+                ts.append(dt)
+        return statistics.mean(ts), res_
+
     if wl["kind"] == "join":
         kv_b, kv_p = KeyVector(bk, br), KeyVector(pk, pr)
         h2d = 12 * (len(bk) + len(pk))
-        for i in range(args.warmup + args.steps):
-            barrier()
-            t0 = time.perf_counter()
-            res = device.probe(kv_b, kv_p)
-            dt = time.perf_counter() - t0
-            if i >= args.warmup:
-                e2e_t.append(dt)
-        d2h = 8 * res.payload.match_count
-        e2e_units = units
     else:
         kv = KeyVector(keys, rows)
         h2d = 12 * len(keys)
-        for i in range(args.warmup + args.steps):
-            barrier()
-            t0 = time.perf_counter()
-            res = device.topk(kv, wl["k"])
-            dt = time.perf_counter() - t0
-            if i >= args.warmup:
-                e2e_t.append(dt)
-        d2h = 4 * len(res.payload.rows)
-        e2e_units = units
+    staged_s, _ = e2e_run(B200Device(device=local, pin_inputs=False)) if not big else (float("nan"), None)
+    e2e_mean, res = e2e_run(device)
+    e2e_t = [e2e_mean]
+    d2h = 8 * res.payload.match_count if wl["kind"] == "join" else 4 * len(res.payload.rows)
+    e2e_units = units
     e2e_s = max_over_ranks(statistics.mean(e2e_t))
     e2e_value = e2e_units / e2e_s / 1e9
+    staged_s = max_over_ranks(staged_s)
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
@@ -378,6 +383,9 @@ def run_b200(args, wl) -> None:
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
             "e2e": {"value": e2e_value, "unit": "Gkeys/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_s * 1e3,
+                    "input_pinning": "input columns page-locked in place after their 2nd use (PinCache); "
+                                     "results DMA into the pinned result arena",
+                    "staged_value": e2e_units / staged_s / 1e9, "staged_ms_per_step": staged_s * 1e3,
                     "last_ledger_ms": {f: getattr(res.ledger, f) * 1e3 for f in ("t_h2d", "t_kernel", "t_d2h",
                                                                                   "t_post")}},
             "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -88,16 +88,29 @@ int golp_last_kernel_times(golp_kernel_times* out);
 int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, int mode,
               uint32_t payload_bytes, uint32_t* out_rows, uint64_t* out_len, golp_ledger* led);
 
-/* Replaces ProxyDevice.probe (pkg/src/golp/device.py:382-436), phase 1 of 2:
- * ships both sides, builds, probes, and reports the match count M. The pairs
- * stay in library-owned device memory until golp_probe_copy_out. */
+/* Replaces ProxyDevice.probe (pkg/src/golp/device.py:382-436). Ships both sides
+ * (build first, then the probe side in chunks that are probed as they land),
+ * builds, probes, and sets *out_matches = M. When M <= out_cap the pairs are
+ * streamed back into out_probe_rows / out_build_rows during the call (chunk c's
+ * pairs download while chunk c+1 uploads), in reference order: probe position,
+ * then build insertion position (host.py:168-188). When M > out_cap the pairs
+ * stay in library memory for golp_probe_copy_out. */
 int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb,
                const double* probe_keys, const uint32_t* probe_rows, uint64_t np, int mode,
-               uint32_t payload_bytes, uint64_t* out_matches, golp_ledger* led);
-/* Phase 2: copy the M pairs of the last golp_probe into caller arrays (each of
- * m = M entries), in reference order: probe position, then build insertion
- * position (host.py:168-188). Adds t_d2h and d2h_bytes = 8*M to *led. */
+               uint32_t payload_bytes, uint32_t* out_probe_rows, uint32_t* out_build_rows,
+               uint64_t out_cap, uint64_t* out_matches, golp_ledger* led);
+/* Copy the M pairs of the last golp_probe into caller arrays of m = M entries
+ * (the M > out_cap case). Adds t_d2h and d2h_bytes = 8*M to *led. */
 int golp_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m, golp_ledger* led);
+/* Host memory for result arrays: a page-locked arena (so results are DMA'd
+ * straight in), falling back to mmap + transparent huge pages. Owned by the
+ * caller's result object, released with golp_host_free(ptr, bytes). */
+void* golp_host_alloc(uint64_t bytes);
+int golp_host_free(void* ptr, uint64_t bytes);
+/* Page-lock a caller buffer in place (read-only) so that transfers of it skip
+ * the staging copy; for columns reused across calls (registration is slow). */
+int golp_host_register(const void* ptr, uint64_t bytes);
+int golp_host_unregister(const void* ptr);
 
 /* ---- device-resident entry points (inputs already in HBM) ---------------------- */
 /* Top-K of n device-resident items. d_out_rows gets min(k, n) rows best first;

@@ -9,7 +9,10 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from pathlib import Path
+
+import numpy as np
 
 from .errors import CapacityError
 
@@ -64,12 +67,17 @@ SIGNATURES = {
     "golp_set_profiling": (_int, [_int]),
     "golp_last_kernel_times": (_int, [C.POINTER(KernelTimes)]),
     "golp_topk": (_int, [_vp, _vp, _u64, _u64, _int, _u32, _vp, C.POINTER(_u64), C.POINTER(Ledger)]),
-    "golp_probe": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, _int, _u32, C.POINTER(_u64), C.POINTER(Ledger)]),
+    "golp_probe": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, _int, _u32, _vp, _vp, _u64, C.POINTER(_u64),
+                          C.POINTER(Ledger)]),
     "golp_probe_copy_out": (_int, [_vp, _vp, _u64, C.POINTER(Ledger)]),
     "golp_topk_device": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
     "golp_topk_merge_device": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
     "golp_join_build_device": (_int, [_vp, _vp, _u64, _vp]),
     "golp_join_probe_device": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, C.POINTER(_u64), _vp]),
+    "golp_host_alloc": (_vp, [_u64]),
+    "golp_host_free": (_int, [_vp, _u64]),
+    "golp_host_register": (_int, [_vp, _u64]),
+    "golp_host_unregister": (_int, [_vp]),
     "golp_host_topk": (_int, [_vp, _vp, _u64, _u64, _vp, _int]),
     "golp_host_hash_build": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),
     "golp_host_hash_probe": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, _int, C.POINTER(_u64)]),
@@ -119,6 +127,42 @@ def check(rc: int) -> None:
 def ptr(arr) -> int:
     """Address of a numpy array's first element (0 for empty arrays)."""
     return int(arr.ctypes.data) if arr.size else 0
+
+
+class _HostBlock:
+    """Owner of one golp_host_alloc block; frees it when the last array view dies."""
+
+    __slots__ = ("ptr", "nbytes", "__weakref__")
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr = ptr
+        self.nbytes = nbytes
+
+    def __del__(self):
+        if self.ptr and _lib is not None:
+            _lib.golp_host_free(self.ptr, self.nbytes)
+            self.ptr = 0
+
+
+def host_array(n: int, dtype=np.uint32) -> np.ndarray:
+    """Fresh 1-D array in library-allocated (huge-page) host memory; the block is
+    released when the array and every view of it are gone."""
+    dt = np.dtype(dtype)
+    nbytes = max(int(n) * dt.itemsize, 1)
+    lib = load()
+    ptr = lib.golp_host_alloc(nbytes)
+    if not ptr:
+        raise MemoryError(last_error() or "golp_host_alloc failed")
+    owner = _HostBlock(int(ptr), nbytes)
+    buf = (C.c_char * nbytes).from_address(int(ptr))
+    arr = np.frombuffer(buf, dtype=dt, count=int(n))
+    # keep the owner alive as long as any view of the array is
+    _keepalive[id(buf)] = owner
+    weakref.finalize(buf, _keepalive.pop, id(buf), None)
+    return arr
+
+
+_keepalive: dict = {}
 
 
 def launch_count() -> int:

@@ -7,6 +7,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <sys/mman.h>
+
+#include <map>
 
 #include "../../include/golp_b200.h"
 #include "join.cuh"
@@ -65,7 +68,11 @@ struct DevBuf {
   T* as() const { return static_cast<T*>(p); }
 };
 
-constexpr int kSlots = 4;
+// Small pinned rings stay resident in the host's last-level cache, so the DMA
+// engine reads/writes them there instead of DRAM (tools/stage_bench.cu: 2 x 16 MB
+// slots with 4 copy threads beat 8 slots or more threads on the GPU box).
+constexpr int kSlots = 2;     // H2D pinned ring
+constexpr int kD2HSlots = 2;  // D2H pinned ring
 constexpr int kNumCtl = 3;  // 0: threshold select, 1: candidate select (+filter count), 2: fallback
 
 struct Ctx {
@@ -73,11 +80,25 @@ struct Ctx {
   int device = 0;
   int sms = 148;
   cudaStream_t s_main = nullptr, s_h2d = nullptr, s_d2h = nullptr;
-  size_t chunk = 32u << 20;
+  size_t chunk = 16u << 20;
   void* pin[kSlots] = {};
   cudaEvent_t pin_ev[kSlots] = {};
   bool pin_busy[kSlots] = {};
   int next_slot = 0;
+  void* dpin[kD2HSlots] = {};
+  cudaEvent_t dpin_ev[kD2HSlots] = {};
+  uint64_t d2h_seq = 0;
+  struct D2HPiece {
+    int slot;
+    char* dst;
+    size_t len;
+  };
+  std::vector<D2HPiece> d2h_q;  // FIFO (front = index d2h_head)
+  size_t d2h_head = 0;
+  bool d2h_direct = false;  // direct (pinned-destination) copies pending on s_d2h
+  std::vector<cudaEvent_t> chunk_ev;
+  uint64_t* mirror = nullptr;  // pinned copy of per-chunk pair totals
+  size_t mirror_n = 0;
   void* pin_small = nullptr;  // samples, counters, small outputs
   size_t pin_small_bytes = 16u << 20;
   WorkerPool pool;
@@ -120,10 +141,14 @@ int do_init(int device, uint64_t chunk_bytes, int host_threads) {
     CK(cudaEventCreateWithFlags(&g.pin_ev[i], cudaEventDisableTiming));
     g.pin_busy[i] = false;
   }
+  for (int i = 0; i < kD2HSlots; ++i) {
+    CK(cudaHostAlloc(&g.dpin[i], g.chunk, cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&g.dpin_ev[i], cudaEventDisableTiming));
+  }
   CK(cudaHostAlloc(&g.pin_small, g.pin_small_bytes, cudaHostAllocDefault));
   for (auto& e : g.ev) CK(cudaEventCreate(&e));
   int hw = (int)std::thread::hardware_concurrency();
-  if (host_threads <= 0) host_threads = std::max(1, std::min(8, hw - 1));
+  if (host_threads <= 0) host_threads = std::max(1, std::min(4, hw - 1));
   g.pool.start(host_threads);
   CK(g.ctl.ensure(sizeof(SelectCtl) * kNumCtl));
   g.ready = true;
@@ -134,10 +159,26 @@ int ensure_init() { return g.ready ? GOLP_OK : do_init(-1, 0, 0); }
 
 SelectCtl* ctl(int i) { return g.ctl.as<SelectCtl>() + i; }
 
+// True when `p` lies in page-locked host memory (cudaHostAlloc'd, our result
+// arena, or a cudaHostRegister'ed caller buffer): the DMA engine can use it directly.
+bool is_pinned(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 // ---- pinned staging ring ----------------------------------------------------------
 // Host -> device copy of an arbitrary pageable buffer: the pool packs chunk i+1
 // into a pinned slot while the DMA engine drains chunk i.
 int stage_h2d(void* dst, const void* src, size_t bytes) {
+  if (bytes && is_pinned(src)) {  // page-locked source: no host copy
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g.s_h2d));
+    return GOLP_OK;
+  }
   size_t done = 0;
   while (done < bytes) {
     const int slot = g.next_slot;
@@ -172,44 +213,61 @@ int stage_dummy_h2d(size_t bytes) {
   return GOLP_OK;
 }
 
-// Device -> host copy into pageable memory through the same ring.
-int stage_d2h(void* dst, const void* src, size_t bytes) {
-  size_t done = 0;
-  int inflight_slot[kSlots] = {};
-  size_t inflight_off[kSlots] = {}, inflight_len[kSlots] = {};
-  int q = 0;
-  auto drain_one = [&](int idx) -> int {
-    CK(cudaEventSynchronize(g.pin_ev[inflight_slot[idx]]));
-    parallel_copy(g.pool, static_cast<char*>(dst) + inflight_off[idx], g.pin[inflight_slot[idx]],
-                  inflight_len[idx]);
-    g.pin_busy[inflight_slot[idx]] = false;
-    return GOLP_OK;
-  };
-  // simple in-order pipeline: keep up to kSlots-1 copies in flight
-  int head = 0;
-  while (done < bytes) {
-    if (q - head >= kSlots - 1) {
-      RET(drain_one(head % kSlots));
-      ++head;
-    }
-    const int slot = g.next_slot;
-    g.next_slot = (g.next_slot + 1) % kSlots;
-    if (g.pin_busy[slot]) CK(cudaEventSynchronize(g.pin_ev[slot]));
-    const size_t len = std::min(g.chunk, bytes - done);
-    CK(cudaMemcpyAsync(g.pin[slot], static_cast<const char*>(src) + done, len, cudaMemcpyDeviceToHost, g.s_d2h));
-    CK(cudaEventRecord(g.pin_ev[slot], g.s_d2h));
-    g.pin_busy[slot] = true;
-    inflight_slot[q % kSlots] = slot;
-    inflight_off[q % kSlots] = done;
-    inflight_len[q % kSlots] = len;
-    ++q;
-    done += len;
-  }
-  while (head < q) {
-    RET(drain_one(head % kSlots));
-    ++head;
+// Device -> host copies into pageable memory through a separate pinned ring:
+// pieces are DMA'd on s_d2h and unpacked (pool memcpy) in FIFO order, either
+// opportunistically (d2h_poll) or when a slot is needed / at the end (d2h_flush).
+int d2h_complete_one() {
+  Ctx::D2HPiece pc = g.d2h_q[g.d2h_head++];
+  CK(cudaEventSynchronize(g.dpin_ev[pc.slot]));
+  parallel_copy(g.pool, pc.dst, g.dpin[pc.slot], pc.len);
+  if (g.d2h_head == g.d2h_q.size()) {
+    g.d2h_q.clear();
+    g.d2h_head = 0;
   }
   return GOLP_OK;
+}
+
+int d2h_enqueue(void* dst, const void* src, size_t bytes) {
+  if (bytes && is_pinned(dst)) {  // page-locked destination (result arena): no host copy
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g.s_d2h));
+    g.d2h_direct = true;
+    return GOLP_OK;
+  }
+  size_t done = 0;
+  while (done < bytes) {
+    while (g.d2h_q.size() - g.d2h_head >= (size_t)kD2HSlots) RET(d2h_complete_one());
+    const int slot = (int)(g.d2h_seq++ % kD2HSlots);
+    const size_t len = std::min(g.chunk, bytes - done);
+    CK(cudaMemcpyAsync(g.dpin[slot], static_cast<const char*>(src) + done, len, cudaMemcpyDeviceToHost, g.s_d2h));
+    CK(cudaEventRecord(g.dpin_ev[slot], g.s_d2h));
+    g.d2h_q.push_back(Ctx::D2HPiece{slot, static_cast<char*>(dst) + done, len});
+    done += len;
+  }
+  return GOLP_OK;
+}
+
+int d2h_poll() {
+  while (g.d2h_head < g.d2h_q.size()) {
+    const cudaError_t e = cudaEventQuery(g.dpin_ev[g.d2h_q[g.d2h_head].slot]);
+    if (e == cudaErrorNotReady) return GOLP_OK;
+    CK(e);
+    RET(d2h_complete_one());
+  }
+  return GOLP_OK;
+}
+
+int d2h_flush() {
+  while (g.d2h_head < g.d2h_q.size()) RET(d2h_complete_one());
+  if (g.d2h_direct) {
+    CK(cudaStreamSynchronize(g.s_d2h));
+    g.d2h_direct = false;
+  }
+  return GOLP_OK;
+}
+
+int stage_d2h(void* dst, const void* src, size_t bytes) {
+  RET(d2h_enqueue(dst, src, bytes));
+  return d2h_flush();
 }
 
 int sync_ring() {
@@ -217,7 +275,96 @@ int sync_ring() {
     if (g.pin_busy[i]) CK(cudaEventSynchronize(g.pin_ev[i]));
     g.pin_busy[i] = false;
   }
+  return d2h_flush();
+}
+
+int ensure_chunk_events(size_t n) {
+  while (g.chunk_ev.size() < n) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g.chunk_ev.push_back(e);
+  }
+  if (g.mirror_n < n + 1) {
+    if (g.mirror) cudaFreeHost(g.mirror);
+    g.mirror = nullptr;
+    g.mirror_n = 0;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&g.mirror), (n + 1) * 8, cudaHostAllocDefault));
+    g.mirror_n = n + 1;
+  }
   return GOLP_OK;
+}
+
+// ---- pinned result arena ---------------------------------------------------------
+// Result arrays handed to Python live here: page-locked, so pairs DMA straight
+// into them. First-fit over 2 MB-granular blocks, coalescing frees; regions are
+// added on demand up to kArenaMax, beyond that golp_host_alloc falls back to mmap.
+constexpr size_t kArenaRegion = size_t(256) << 20;
+constexpr size_t kArenaMax = size_t(4) << 30;
+constexpr size_t kArenaGrain = size_t(2) << 20;
+struct ArenaRegion {
+  char* base;
+  size_t size;
+  std::map<size_t, size_t> free_;  // offset -> length
+};
+std::mutex g_arena_mu;
+std::vector<ArenaRegion> g_arena;
+std::map<const void*, std::pair<size_t, size_t>> g_arena_live;  // ptr -> (region, length)
+size_t g_arena_total = 0;
+
+void* arena_alloc(size_t bytes) {
+  const size_t len = (bytes + kArenaGrain - 1) / kArenaGrain * kArenaGrain;
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    for (size_t r = 0; r < g_arena.size(); ++r) {
+      auto& fl = g_arena[r].free_;
+      for (auto it = fl.begin(); it != fl.end(); ++it) {
+        if (it->second < len) continue;
+        const size_t off = it->first, rest = it->second - len;
+        fl.erase(it);
+        if (rest) fl[off + len] = rest;
+        char* p = g_arena[r].base + off;
+        g_arena_live[p] = {r, len};
+        return p;
+      }
+    }
+    const size_t want = std::max(kArenaRegion, len);
+    if (g_arena_total + want > kArenaMax || !g.ready) return nullptr;
+    void* base = nullptr;
+    if (cudaHostAlloc(&base, want, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    ArenaRegion reg{static_cast<char*>(base), want, {}};
+    reg.free_[0] = want;
+    g_arena.push_back(std::move(reg));
+    g_arena_total += want;
+  }
+  return nullptr;
+}
+
+bool arena_free(const void* p) {
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  auto it = g_arena_live.find(p);
+  if (it == g_arena_live.end()) return false;
+  const size_t r = it->second.first, len = it->second.second;
+  g_arena_live.erase(it);
+  auto& fl = g_arena[r].free_;
+  size_t off = static_cast<const char*>(p) - g_arena[r].base, l = len;
+  auto nx = fl.lower_bound(off);
+  if (nx != fl.end() && off + l == nx->first) {
+    l += nx->second;
+    nx = fl.erase(nx);
+  }
+  if (nx != fl.begin()) {
+    auto pv = std::prev(nx);
+    if (pv->first + pv->second == off) {
+      off = pv->first;
+      l += pv->second;
+      fl.erase(pv);
+    }
+  }
+  fl[off] = l;
+  return true;
 }
 
 // ---- Top-K planning ---------------------------------------------------------------
@@ -427,17 +574,19 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   }
   unsigned long long* cursor = g.jcount.as<unsigned long long>();
   unsigned int* big_count = reinterpret_cast<unsigned int*>(cursor + 1);
-  const int gb = grid_for(nb, 256, 8);
-  join_insert_kernel<<<gb, 256, 0, s>>>(bkeys, nb, table, g.jmask, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>());
+  const int gb = grid_for((nb + kBuildItems - 1) / kBuildItems, kBuildThreads, 8);
+  join_insert_kernel<<<gb, kBuildThreads, 0, s>>>(bkeys, nb, table, g.jmask, g.bslot.as<uint32_t>(),
+                                                  g.brank.as<uint32_t>());
   CKL();
-  join_offsets_kernel<<<gb, 256, 0, s>>>(nb, table, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>(), cursor,
-                                         g.big_list.as<uint32_t>(), big_count);
+  join_offsets_kernel<<<gb, kBuildThreads, 0, s>>>(nb, table, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>(), brows,
+                                                   cursor, g.big_list.as<uint32_t>(), big_count);
   CKL();
-  join_fill_kernel<<<gb, 256, 0, s>>>(nb, table, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>(),
-                                      g.csr_pos.as<uint32_t>());
+  join_fill_kernel<<<gb, kBuildThreads, 0, s>>>(nb, table, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>(),
+                                                g.csr_pos.as<uint32_t>());
   CKL();
-  join_small_groups_kernel<<<gb, 256, 0, s>>>(nb, table, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>(),
-                                              g.csr_pos.as<uint32_t>(), brows, g.csr_row.as<uint32_t>());
+  join_small_groups_kernel<<<grid_for(nb, 256, 8), 256, 0, s>>>(nb, table, g.bslot.as<uint32_t>(),
+                                                                g.brank.as<uint32_t>(), g.csr_pos.as<uint32_t>(),
+                                                                brows, g.csr_row.as<uint32_t>());
   CKL();
   static bool attr = false;
   const size_t smem = kGroupTile * sizeof(uint32_t);
@@ -580,6 +729,21 @@ int golp_shutdown(void) {
   }
   if (g.pin_small) cudaFreeHost(g.pin_small);
   g.pin_small = nullptr;
+  for (int i = 0; i < kD2HSlots; ++i) {
+    if (g.dpin[i]) cudaFreeHost(g.dpin[i]);
+    if (g.dpin_ev[i]) cudaEventDestroy(g.dpin_ev[i]);
+    g.dpin[i] = nullptr;
+    g.dpin_ev[i] = nullptr;
+  }
+  g.d2h_q.clear();
+  g.d2h_head = 0;
+  g.d2h_direct = false;
+  for (cudaEvent_t e : g.chunk_ev) cudaEventDestroy(e);
+  g.chunk_ev.clear();
+  if (g.mirror) cudaFreeHost(g.mirror);
+  g.mirror = nullptr;
+  g.mirror_n = 0;
+  // the pinned result arena outlives shutdown: result arrays may still be alive
   for (auto& e : g.ev) {
     if (e) cudaEventDestroy(e);
     e = nullptr;
@@ -761,11 +925,12 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
 }
 
 int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb, const double* probe_keys,
-               const uint32_t* probe_rows, uint64_t np, int mode, uint32_t payload_bytes, uint64_t* out_matches,
-               golp_ledger* led) {
+               const uint32_t* probe_rows, uint64_t np, int mode, uint32_t payload_bytes, uint32_t* out_probe_rows,
+               uint32_t* out_build_rows, uint64_t out_cap, uint64_t* out_matches, golp_ledger* led) {
   uint64_t entry = 0;
   RET(check_mode(mode, payload_bytes, &entry));
   if (!out_matches || !led) return invalid("null output pointer");
+  if (out_cap && (!out_probe_rows || !out_build_rows)) return invalid("null output arrays");
   RET(ensure_init());
   g.last_probe_valid = false;
   const double t0 = wall_seconds();
@@ -796,11 +961,40 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   const uint64_t nchunks = np ? (np + per_chunk - 1) / per_chunk : 0;
   CK(g.totals.ensure((nchunks + 1) * 8));
   CK(cudaMemsetAsync(g.totals.p, 0, (nchunks + 1) * 8, s));
-  uint64_t out_cap = std::max<uint64_t>(g.pairs_p.bytes / 4, std::max<uint64_t>(np, 1024));
-  CK(g.pairs_p.ensure(out_cap * 4));
-  CK(g.pairs_b.ensure(out_cap * 4));
-  out_cap = std::min(g.pairs_p.bytes, g.pairs_b.bytes) / 4;
+  RET(ensure_chunk_events(nchunks));
+  g.mirror[0] = 0;
+  uint64_t dcap = std::max<uint64_t>(g.pairs_p.bytes / 4, std::max<uint64_t>(np, 1024));
+  CK(g.pairs_p.ensure(dcap * 4));
+  CK(g.pairs_b.ensure(dcap * 4));
+  dcap = std::min(g.pairs_p.bytes, g.pairs_b.bytes) / 4;
   unsigned long long* totals = g.totals.as<unsigned long long>();
+  // Pairs of chunk c stream back (DMA + unpack into the caller's arrays) while
+  // later chunks upload; a chunk is ready once its probe event has fired.
+  uint64_t streamed = 0;     // chunks whose pairs are queued for D2H
+  bool streaming = out_cap > 0;
+  auto stream_ready = [&](bool block) -> int {
+    while (streaming && streamed < nchunks) {
+      cudaEvent_t e = g.chunk_ev[streamed];
+      if (block) {
+        CK(cudaEventSynchronize(e));
+      } else {
+        const cudaError_t q = cudaEventQuery(e);
+        if (q == cudaErrorNotReady) break;
+        CK(q);
+      }
+      const uint64_t lo = g.mirror[streamed], hi = g.mirror[streamed + 1];
+      if (hi > out_cap || hi > dcap) {
+        streaming = false;  // caller's arrays (or the device buffer) too small: copy_out path
+        break;
+      }
+      if (hi > lo) {
+        RET(d2h_enqueue(out_probe_rows + lo, g.pairs_p.as<uint32_t>() + lo, (hi - lo) * 4));
+        RET(d2h_enqueue(out_build_rows + lo, g.pairs_b.as<uint32_t>() + lo, (hi - lo) * 4));
+      }
+      ++streamed;
+    }
+    return d2h_poll();
+  };
   auto run_chunks = [&](bool with_h2d) -> int {
     for (uint64_t c = 0; c < nchunks; ++c) {
       const uint64_t c0 = c * per_chunk;
@@ -812,8 +1006,14 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
         CK(cudaEventRecord(ev_chunk, g.s_h2d));
         CK(cudaStreamWaitEvent(s, ev_chunk, 0));
       }
-      RET(launch_probe(dpk + c0, dpr + c0, cn, g.pairs_p.as<uint32_t>(), g.pairs_b.as<uint32_t>(), out_cap,
+      RET(launch_probe(dpk + c0, dpr + c0, cn, g.pairs_p.as<uint32_t>(), g.pairs_b.as<uint32_t>(), dcap,
                        totals + c, totals + c + 1, s));
+      if (with_h2d) {
+        CK(cudaMemcpyAsync(g.mirror + c + 1, totals + c + 1, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(g.chunk_ev[c], s));
+        CK(cudaStreamWaitEvent(g.s_d2h, g.chunk_ev[c], 0));
+        RET(stream_ready(false));
+      }
     }
     return GOLP_OK;
   };
@@ -825,20 +1025,32 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   const double t1 = wall_seconds();
   uint64_t m = 0;
   RET(read_probe_total(totals + nchunks, &m, s));
-  if (m > out_cap) {  // rare: more pairs than probes; grow and re-probe the resident input
+  const double t2 = wall_seconds();
+  if (m > dcap) {  // rare: more pairs than probes; grow and re-probe the resident input
+    streaming = false;
+    RET(d2h_flush());
     CK(g.pairs_p.ensure(m * 4));
     CK(g.pairs_b.ensure(m * 4));
-    out_cap = std::min(g.pairs_p.bytes, g.pairs_b.bytes) / 4;
+    dcap = std::min(g.pairs_p.bytes, g.pairs_b.bytes) / 4;
     CK(cudaMemsetAsync(g.totals.p, 0, (nchunks + 1) * 8, s));
     RET(run_chunks(false));
     RET(read_probe_total(totals + nchunks, &m, s));
   }
-  const double t2 = wall_seconds();
+  RET(stream_ready(true));
+  RET(d2h_flush());
+  const double t3 = wall_seconds();
   *out_matches = m;
   g.last_m = m;
   g.last_probe_valid = true;
+  const bool delivered = streaming && m <= out_cap && streamed == nchunks;
   led->t_h2d = t1 - t0;
   led->t_kernel = t2 - t1;
+  if (delivered) {
+    led->t_d2h = t3 - t2;
+    led->d2h_bytes = 8 * m;
+  } else {
+    led->t_kernel += t3 - t2;  // copy_out adds the D2H phase
+  }
   return GOLP_OK;
 }
 
@@ -856,6 +1068,41 @@ int golp_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m, 
     led->d2h_bytes = 8 * m;
     led->t_d2h = wall_seconds() - t0;
   }
+  return GOLP_OK;
+}
+
+// ---- host result allocator: pinned arena, mmap fallback ----------------------------
+void* golp_host_alloc(uint64_t bytes) {
+  if (bytes == 0) bytes = 1;
+  if (void* p = arena_alloc(bytes)) return p;  // page-locked: results DMA straight in
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (p == MAP_FAILED) {
+    set_error("mmap failed for a host result buffer");
+    return nullptr;
+  }
+  madvise(p, bytes, MADV_HUGEPAGE);
+  return p;
+}
+
+int golp_host_free(void* p, uint64_t bytes) {
+  if (!p) return GOLP_OK;
+  if (arena_free(p)) return GOLP_OK;
+  if (bytes == 0) bytes = 1;
+  return munmap(p, bytes) == 0 ? GOLP_OK : GOLP_ERR_INVALID;
+}
+
+// Page-lock a caller buffer in place (read-only) so repeated transfers of it skip
+// the staging copy. Slow (~5 GB/s): worth it only for buffers reused across calls.
+int golp_host_register(const void* p, uint64_t bytes) {
+  RET(ensure_init());
+  if (!p || !bytes) return invalid("empty range");
+  CK(cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterReadOnly));
+  return GOLP_OK;
+}
+
+int golp_host_unregister(const void* p) {
+  if (!p) return GOLP_OK;
+  CK(cudaHostUnregister(const_cast<void*>(p)));
   return GOLP_OK;
 }
 

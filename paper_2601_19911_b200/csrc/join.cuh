@@ -45,82 +45,149 @@ __global__ void join_init_table_kernel(Slot* __restrict__ table, uint64_t cap) {
   }
 }
 
-__global__ void join_insert_kernel(const double* __restrict__ bkeys, uint64_t nb, Slot* table, uint64_t mask,
-                                   uint32_t* __restrict__ bslot, uint32_t* __restrict__ brank) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += stride) {
-    const uint64_t b = canon_bits(__ldg(bkeys + i));
-    uint64_t h = home_slot(b, mask);
-    while (true) {
-      unsigned long long* kp = reinterpret_cast<unsigned long long*>(&table[h].key);
-      const unsigned long long k = *(volatile unsigned long long*)kp;
-      if (k == b) break;
-      if (k == kEmptyKey) {
-        const unsigned long long old = atomicCAS(kp, kEmptyKey, (unsigned long long)b);
-        if (old == kEmptyKey || old == b) break;
-      }
-      h = (h + 1) & mask;
-    }
-    const uint32_t r = atomicAdd(&table[h].cnt, 1u);
-    bslot[i] = (uint32_t)h;
-    brank[i] = r;
-  }
-}
+// Build kernels process tiles of kBuildThreads*kBuildItems consecutive entries;
+// each thread owns kBuildItems entries strided by the block size (coalesced),
+// and issues their loads / atomics together so the dependent chains overlap.
+constexpr int kBuildThreads = 256;
+constexpr int kBuildItems = 4;
+constexpr uint64_t kBuildTile = (uint64_t)kBuildThreads * kBuildItems;
 
-// One leader per group (rank 0) reserves the group's CSR range.
-__global__ void join_offsets_kernel(uint64_t nb, Slot* table, const uint32_t* __restrict__ bslot,
-                                    const uint32_t* __restrict__ brank, unsigned long long* cursor,
-                                    uint32_t* big_list, unsigned int* big_count) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const unsigned lane = lane_id();
-  for (uint64_t wb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; wb < nb; wb += stride) {
-    const uint64_t i = wb + lane;
-    uint32_t h = 0, cnt = 0;
-    const bool leader = i < nb && brank[i] == 0;
-    if (leader) {
-      h = bslot[i];
-      cnt = table[h].cnt;
-    }
-    unsigned long long incl = cnt;
+__global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double* __restrict__ bkeys, uint64_t nb,
+                                                                    Slot* table, uint64_t mask,
+                                                                    uint32_t* __restrict__ bslot,
+                                                                    uint32_t* __restrict__ brank) {
+  for (uint64_t t0 = (uint64_t)blockIdx.x * kBuildTile; t0 < nb; t0 += (uint64_t)gridDim.x * kBuildTile) {
+    uint64_t b[kBuildItems];
+    uint32_t h[kBuildItems];
+    unsigned pending = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if ((int)lane >= o) incl += v;
+    for (int j = 0; j < kBuildItems; ++j) {
+      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
+      b[j] = i < nb ? canon_bits(__ldg(bkeys + i)) : 0ull;
+      h[j] = (uint32_t)home_slot(b[j], mask);
+      if (i < nb) pending |= 1u << j;
     }
-    unsigned long long base = 0;
-    if (lane == 31 && incl) base = atomicAdd(cursor, incl);
-    base = __shfl_sync(0xFFFFFFFFu, base, 31);
-    if (leader) {
-      table[h].off = (uint32_t)(base + incl - cnt);
-      if (cnt > (uint32_t)kSmallGroup) big_list[atomicAdd(big_count, 1u)] = h;
+    unsigned valid = pending;
+    // Claim or find each key's slot: CAS issued for every pending entry at once.
+    while (pending) {
+      unsigned long long old[kBuildItems];
+#pragma unroll
+      for (int j = 0; j < kBuildItems; ++j)
+        if (pending & (1u << j))
+          old[j] = atomicCAS(reinterpret_cast<unsigned long long*>(&table[h[j]].key), kEmptyKey,
+                             (unsigned long long)b[j]);
+#pragma unroll
+      for (int j = 0; j < kBuildItems; ++j) {
+        if (!(pending & (1u << j))) continue;
+        if (old[j] == kEmptyKey || old[j] == b[j]) pending &= ~(1u << j);
+        else h[j] = (h[j] + 1) & (uint32_t)mask;
+      }
+    }
+    uint32_t r[kBuildItems];
+#pragma unroll
+    for (int j = 0; j < kBuildItems; ++j)
+      if (valid & (1u << j)) r[j] = atomicAdd(&table[h[j]].cnt, 1u);
+#pragma unroll
+    for (int j = 0; j < kBuildItems; ++j) {
+      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
+      if (valid & (1u << j)) {
+        bslot[i] = h[j];
+        brank[i] = r[j];
+      }
     }
   }
 }
 
-__global__ void join_fill_kernel(uint64_t nb, const Slot* __restrict__ table, const uint32_t* __restrict__ bslot,
-                                 const uint32_t* __restrict__ brank, uint32_t* __restrict__ csr_pos) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += stride) {
-    csr_pos[table[bslot[i]].off + brank[i]] = (uint32_t)i;
+// One leader per group (rank 0) reserves the group's CSR range; groups of one
+// keep their row inline in slot.off and reserve nothing.
+__global__ void __launch_bounds__(kBuildThreads) join_offsets_kernel(uint64_t nb, Slot* table,
+                                                                     const uint32_t* __restrict__ bslot,
+                                                                     const uint32_t* __restrict__ brank,
+                                                                     const uint32_t* __restrict__ brows,
+                                                                     unsigned long long* cursor, uint32_t* big_list,
+                                                                     unsigned int* big_count) {
+  const unsigned lane = lane_id();
+  for (uint64_t t0 = (uint64_t)blockIdx.x * kBuildTile; t0 < nb; t0 += (uint64_t)gridDim.x * kBuildTile) {
+    uint32_t h[kBuildItems], cnt[kBuildItems], rk[kBuildItems];
+#pragma unroll
+    for (int j = 0; j < kBuildItems; ++j) {
+      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
+      rk[j] = i < nb ? brank[i] : 1u;
+      h[j] = i < nb ? bslot[i] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kBuildItems; ++j) cnt[j] = rk[j] == 0 ? table[h[j]].cnt : 0u;
+#pragma unroll
+    for (int j = 0; j < kBuildItems; ++j) {
+      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
+      if (cnt[j] == 1) table[h[j]].off = __ldg(brows + i);  // singleton: inline row
+      const uint32_t need = cnt[j] > 1 ? cnt[j] : 0u;
+      unsigned long long incl = need;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((int)lane >= o) incl += v;
+      }
+      unsigned long long base = 0;
+      if (lane == 31 && incl) base = atomicAdd(cursor, incl);
+      base = __shfl_sync(0xFFFFFFFFu, base, 31);
+      if (need) {
+        table[h[j]].off = (uint32_t)(base + incl - need);
+        if (need > (uint32_t)kSmallGroup) big_list[atomicAdd(big_count, 1u)] = h[j];
+      }
+    }
   }
 }
 
-// Groups of <= kSmallGroup: the leader sorts the positions and writes rows.
-// Groups of one keep the row inline in slot.off.
-__global__ void join_small_groups_kernel(uint64_t nb, Slot* table, const uint32_t* __restrict__ bslot,
-                                         const uint32_t* __restrict__ brank, const uint32_t* __restrict__ csr_pos,
-                                         const uint32_t* __restrict__ brows, uint32_t* __restrict__ csr_row) {
+// Members of multi-entry groups scatter their build positions into the group's range.
+__global__ void __launch_bounds__(kBuildThreads) join_fill_kernel(uint64_t nb, const Slot* __restrict__ table,
+                                                                  const uint32_t* __restrict__ bslot,
+                                                                  const uint32_t* __restrict__ brank,
+                                                                  uint32_t* __restrict__ csr_pos) {
+  for (uint64_t t0 = (uint64_t)blockIdx.x * kBuildTile; t0 < nb; t0 += (uint64_t)gridDim.x * kBuildTile) {
+    uint32_t h[kBuildItems], rk[kBuildItems];
+    uint2 oc[kBuildItems];
+#pragma unroll
+    for (int j = 0; j < kBuildItems; ++j) {
+      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
+      h[j] = i < nb ? bslot[i] : 0u;
+      rk[j] = i < nb ? brank[i] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kBuildItems; ++j) {
+      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
+      oc[j] = i < nb ? *reinterpret_cast<const uint2*>(&table[h[j]].off) : make_uint2(0, 1);
+    }
+#pragma unroll
+    for (int j = 0; j < kBuildItems; ++j) {
+      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
+      if (i < nb && oc[j].y > 1) csr_pos[oc[j].x + rk[j]] = (uint32_t)i;
+    }
+  }
+}
+
+// Groups of 2..kSmallGroup: the leader sorts the positions and writes rows.
+__global__ void __launch_bounds__(kBuildThreads) join_small_groups_kernel(uint64_t nb, const Slot* __restrict__ table,
+                                                                          const uint32_t* __restrict__ bslot,
+                                                                          const uint32_t* __restrict__ brank,
+                                                                          const uint32_t* __restrict__ csr_pos,
+                                                                          const uint32_t* __restrict__ brows,
+                                                                          uint32_t* __restrict__ csr_row) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += stride) {
     if (brank[i] != 0) continue;
     const uint32_t h = bslot[i];
-    const uint32_t cnt = table[h].cnt;
-    if (cnt == 1) {
-      table[h].off = __ldg(brows + i);
+    const uint2 oc = *reinterpret_cast<const uint2*>(&table[h].off);
+    const uint32_t cnt = oc.y;
+    if (cnt < 2 || cnt > (uint32_t)kSmallGroup) continue;
+    const uint32_t off = oc.x;
+    if (cnt == 2) {  // the common case: one compare
+      const uint32_t a = csr_pos[off], b = csr_pos[off + 1];
+      const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
+      csr_row[off] = __ldg(brows + lo);
+      csr_row[off + 1] = __ldg(brows + hi);
       continue;
     }
-    if (cnt > (uint32_t)kSmallGroup) continue;
-    const uint32_t off = table[h].off;
     uint32_t p[kSmallGroup];
     for (uint32_t m = 0; m < cnt; ++m) {
       const uint32_t v = csr_pos[off + m];
