@@ -1,0 +1,159 @@
+"""Gate / cost model / calibration / statistics against the reference's own
+numbers (tests/golden/gate.json, produced by running golp), plus the
+reference's behavioural gate tests restated on this package."""
+
+import math
+
+import numpy as np
+import pytest
+
+from golden_io import gate_golden
+from paper_2601_19911_b200 import (
+    DEFAULT_CPU_MODEL,
+    DEFAULT_MODELED_PROFILE,
+    DEVICE,
+    FULL_ROW,
+    HOST,
+    KEY_ONLY,
+    OP_PROBE,
+    OP_TOPK,
+    CalibrationError,
+    CpuCostModel,
+    DeviceProfile,
+    GateConfig,
+    ModeledDevice,
+    StrategyMismatchError,
+    TransferLedger,
+    calibrate_cpu_model,
+    calibrate_profile,
+    decide,
+    estimate_cpu_cost,
+    estimate_device_cost,
+    execute_gated,
+    generate_table,
+    transfer_entry_bytes,
+    with_margin,
+)
+from paper_2601_19911_b200.harness import (
+    WorkloadSpec,
+    compute_stats,
+    run_payload_comparison,
+    run_strategy_comparison,
+)
+
+G = gate_golden()
+CFGS = {
+    "default": GateConfig(),
+    "margin5ms": GateConfig(margin_s=5e-3),
+    "guard20k": GateConfig(min_n_guard=20_000),
+    "full_row": GateConfig(mode=FULL_ROW),
+}
+
+
+def test_decide_matches_reference_on_every_grid_point():
+    assert len(G["decide"]) > 300
+    for name, op, n, k, build_n, path, c_cpu, c_gpu, gain, guard in G["decide"]:
+        cfg = CFGS[name]
+        pb = 188 if cfg.mode == FULL_ROW else None
+        d = decide(cfg, op, n, k, pb, build_n)
+        assert (d.path, d.guard_triggered) == (path, guard), (name, op, n, k, build_n)
+        assert d.c_cpu_est == c_cpu and d.c_gpu_est == c_gpu and d.gain == gain
+
+
+def test_estimate_device_cost_matches_reference():
+    for op, n, mode, est in G["estimate"]:
+        pb = 188 if mode == FULL_ROW else None
+        assert list(estimate_device_cost(op, n, 100, mode, pb)) == est
+
+
+def test_calibrate_profile_matches_reference():
+    c = G["calibrate_profile"]
+    samples = [(n, TransferLedger(*vals)) for n, vals in c["samples"]]
+    prof = calibrate_profile(samples)
+    for k, v in c["profile"].items():
+        assert getattr(prof, k) == pytest.approx(v, rel=1e-12)
+
+
+def test_calibrate_cpu_model_matches_reference():
+    c = G["calibrate_cpu"]
+    model = calibrate_cpu_model([tuple(s) for s in c["samples"]])
+    for k, v in c["model"].items():
+        assert getattr(model, k) == pytest.approx(v, rel=1e-12)
+
+
+def test_compute_stats_nearest_rank_matches_reference():
+    for seq, med, p95, p99, mean in G["stats"]:
+        s = compute_stats(seq)
+        assert (s.median, s.p95, s.p99) == (med, p95, p99)
+        assert s.mean == pytest.approx(mean, rel=1e-15)
+
+
+def test_strict_gain_and_guard_rules():
+    flat_cpu = CpuCostModel(0.0, 10e-3, 0.0, 10e-3)
+    flat_dev = DeviceProfile(1e15, 1e15, 4e-3, 1e-15, 1e-15, 1e-15)
+    cfg = GateConfig(cpu_model=flat_cpu, profile=flat_dev)
+    assert decide(with_margin(cfg, 5e-3), OP_TOPK, 1000, 100).path == DEVICE
+    assert decide(with_margin(cfg, 10e-3), OP_TOPK, 1000, 100).path == HOST
+    d = decide(GateConfig(cpu_model=flat_cpu, profile=flat_dev, min_n_guard=5000), OP_TOPK, 1000, 100)
+    assert d.guard_triggered and d.path == HOST
+    # probes charge both sides to the device
+    a = decide(GateConfig(), OP_PROBE, 1000, 1, None, 0).c_gpu_est
+    b = decide(GateConfig(), OP_PROBE, 1000, 1, None, 10**6).c_gpu_est
+    assert b > a
+
+
+def test_validation_errors_like_the_reference():
+    with pytest.raises(ValueError):
+        GateConfig(margin_s=-1.0)
+    with pytest.raises(ValueError):
+        GateConfig(mode="bogus")
+    with pytest.raises(ValueError):
+        transfer_entry_bytes(FULL_ROW, None)
+    with pytest.raises(ValueError):
+        DeviceProfile(0.0, 1.0, 1.0, 1.0, 1.0, 1.0)
+    with pytest.raises(ValueError):
+        estimate_cpu_cost(DEFAULT_CPU_MODEL, "bogus", 10)
+    with pytest.raises(CalibrationError):
+        calibrate_profile([(10, TransferLedger.build(1, 1, 1.0, 1.0, 1.0, 1.0))] * 3)
+    cfg = GateConfig.from_json_dict(GateConfig(margin_s=1e-3, min_n_guard=7).to_json_dict())
+    assert cfg == GateConfig(margin_s=1e-3, min_n_guard=7)
+    assert DeviceProfile.from_json_dict(DEFAULT_MODELED_PROFILE.to_json_dict()) == DEFAULT_MODELED_PROFILE
+
+
+def test_modeled_e2e_speedup_at_3m_matches_reference_story():
+    cmp = run_payload_comparison(WorkloadSpec(n_grid=(3_000_000,), repeats=1))
+    full = next(r for r in cmp.e2e_rows if r.mode == FULL_ROW)
+    key = next(r for r in cmp.e2e_rows if r.mode == KEY_ONLY)
+    assert full.e2e_s == pytest.approx(2.4020016e-2, rel=1e-6)
+    assert key.e2e_s == pytest.approx(1.942016e-3, rel=1e-6)
+    assert key.speedup_vs_full_row == pytest.approx(12.368598, rel=1e-6)
+
+
+def test_gated_mixed_workload_wins_the_tail_modeled():
+    spec = WorkloadSpec(n_grid=(10_000, 1_000_000), repeats=250, mix=(0.8, 0.2), seed=3)
+    host, device, gated = run_strategy_comparison(spec, GateConfig())
+    hs, ds, gs = (compute_stats(r.all_samples()) for r in (host, device, gated))
+    assert gs.p95 <= hs.p95 and gs.p95 <= ds.p95 and gs.p99 <= ds.p99
+    assert 0.0 < gated.offload_rate < 1.0
+
+
+class _LyingDevice(ModeledDevice):
+    def topk(self, keys, k, mode=KEY_ONLY, payload_bytes=None):
+        call = super().topk(keys, k, mode=mode, payload_bytes=payload_bytes)
+        call.payload.rows[:] = call.payload.rows[::-1]
+        return call
+
+
+def test_divergent_answers_abort_the_comparison():
+    spec = WorkloadSpec(n_grid=(1_000, 10_000), repeats=2)
+    with pytest.raises(StrategyMismatchError):
+        run_strategy_comparison(spec, GateConfig(), device=_LyingDevice())
+
+
+def test_execute_gated_topk_and_probe_on_host_path():
+    t = generate_table(5000, 16, seed=3)
+    res, d, lat = execute_gated(t, OP_TOPK, 10, GateConfig())
+    assert d.path == HOST and len(res) == 10 and lat > 0
+    assert np.all(np.diff(res.keys) <= 0)
+    res2, d2, _ = execute_gated((generate_table(300, 8, seed=1), t), OP_PROBE, 1, GateConfig())
+    assert d2.path == HOST and res2.probe_count == 5000

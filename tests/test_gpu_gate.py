@@ -1,0 +1,47 @@
+"""Risky Gate with the B200 backend: calibrated profile from real ledgers,
+strategy comparison (answers cross-checked between the host engine and the
+device on every query), gated execution of both ops."""
+
+import numpy as np
+import pytest
+
+from paper_2601_19911_b200 import DEVICE, HOST, OP_PROBE, OP_TOPK, GateConfig, execute_gated, execute_path, generate_table
+from paper_2601_19911_b200.harness import (
+    WorkloadSpec,
+    calibrate_device_profile,
+    compute_stats,
+    run_strategy_comparison,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def test_b200_profile_calibrates_and_strategies_agree(b200):
+    prof = calibrate_device_profile(b200, ns=(50_000, 200_000, 800_000, 2_000_000), repeats=2)
+    assert prof.h2d_bandwidth > 1e9 and prof.launch_overhead > 0
+    cfg = GateConfig(profile=prof, min_n_guard=20_000)
+    spec = WorkloadSpec(n_grid=(10_000, 100_000, 1_000_000), repeats=3, payload_bytes=16, k=100)
+    host, device, gated = run_strategy_comparison(spec, cfg, device=b200)  # raises on any mismatch
+    assert device.offload_rate == 1.0 and host.offload_rate == 0.0
+    for run in (host, device, gated):
+        s = compute_stats(run.all_samples())
+        assert s.p99 >= s.p95 >= s.median > 0
+
+
+def test_device_and_host_paths_return_identical_results(b200):
+    t = generate_table(300_000, 8, seed=5)
+    cfg = GateConfig()
+    r_dev, _ = execute_path(t, OP_TOPK, 1000, cfg, b200, DEVICE)
+    r_host, _ = execute_path(t, OP_TOPK, 1000, cfg, b200, HOST)
+    assert np.array_equal(r_dev.row_ids, r_host.row_ids)
+    assert np.array_equal(r_dev.payloads, r_host.payloads)
+    bt = generate_table(50_000, 8, seed=6)
+    p_dev, _ = execute_path((bt, t), OP_PROBE, 1, cfg, b200, DEVICE)
+    p_host, _ = execute_path((bt, t), OP_PROBE, 1, cfg, b200, HOST)
+    assert p_dev.matches == p_host.matches
+
+
+def test_execute_gated_offloads_large_queries(b200):
+    t = generate_table(3_000_000, 4, seed=2)
+    res, d, lat = execute_gated(t, OP_TOPK, 100, GateConfig(), device=b200)
+    assert d.path == DEVICE and len(res) == 100 and lat > 0

@@ -1,0 +1,66 @@
+"""Config C5 (BASELINE.json): Risky Gate sweep on the B200. Calibrates the
+DeviceProfile from B200 ledgers and the CpuCostModel from host-engine timings,
+then reports decide() under the reference's default constants next to the
+calibrated ones over N x K x mode, and P50/P95/P99 of host_only /
+device_always / gated on the reference's 80/20 mixed stream (crit 7 shape).
+
+    python tools/gate_sweep.py [out.json]
+"""
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+from paper_2601_19911_b200 import (  # noqa: E402
+    B200Device, FULL_ROW, KEY_ONLY, OP_TOPK, GateConfig, calibrate_cpu_model, decide, host_topk, random_key_vector)
+from paper_2601_19911_b200.harness import (  # noqa: E402
+    WorkloadSpec, calibrate_device_profile, compute_stats, run_strategy_comparison)
+
+
+def main(out_path):
+    dev = B200Device()
+    t0 = time.time()
+    prof = calibrate_device_profile(dev, ns=(100_000, 1_000_000, 4_000_000, 16_000_000), repeats=3,
+                                    probe_ns=(200_000, 2_000_000, 8_000_000))
+    cpu_samples = []
+    for n in (100_000, 1_000_000, 4_000_000, 16_000_000):
+        kv = random_key_vector(n, n)
+        host_topk(kv, 100)
+        ts = []
+        for _ in range(3):
+            a = time.perf_counter()
+            host_topk(kv, 100)
+            ts.append(time.perf_counter() - a)
+        cpu_samples.append((OP_TOPK, n, 100, sorted(ts)[1]))
+    cpu = calibrate_cpu_model(cpu_samples)
+    ref_cfg = GateConfig()
+    cal_cfg = GateConfig(profile=prof, cpu_model=cpu)
+    grid = []
+    for n in (1_000, 10_000, 20_000, 100_000, 1_000_000, 10_000_000, 100_000_000, 1_000_000_000):
+        for k in (10, 100, 1000, 100_000):
+            for mode in (KEY_ONLY, FULL_ROW):
+                pb = 188 if mode == FULL_ROW else None
+                r = decide(GateConfig(mode=mode), OP_TOPK, n, k, pb)
+                c = decide(GateConfig(mode=mode, profile=prof, cpu_model=cpu), OP_TOPK, n, k, pb)
+                grid.append({"n": n, "k": k, "mode": mode, "reference_decision": r.path, "reference_gain_s": r.gain,
+                             "calibrated_decision": c.path, "calibrated_gain_s": c.gain,
+                             "c_gpu_calibrated_s": c.c_gpu_est, "c_cpu_calibrated_s": c.c_cpu_est})
+    strat = {}
+    for label, cfg in (("reference_constants", ref_cfg), ("calibrated", cal_cfg)):
+        spec = WorkloadSpec(n_grid=(10_000, 1_000_000), repeats=100, mix=(0.8, 0.2), seed=3, payload_bytes=16)
+        runs = run_strategy_comparison(spec, cfg, device=dev)
+        strat[label] = {r.strategy: {**{k: getattr(compute_stats(r.all_samples()), k) for k in ("median", "p95", "p99")},
+                                     "offload_rate": r.offload_rate} for r in runs}
+    out = {"profile_b200": prof.to_json_dict(), "cpu_model_host_engine": cpu.to_json_dict(),
+           "decisions": grid, "strategy_80_20_stream": strat, "wall_s": time.time() - t0}
+    Path(out_path).write_text(json.dumps(out, indent=1))
+    print(json.dumps({"profile": out["profile_b200"], "strategies": strat}, indent=1))
+    dev.close()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/gate_sweep.json")
