@@ -17,7 +17,7 @@ from typing import NamedTuple, Optional, Sequence
 
 import numpy as np
 
-from .device import DEFAULT_MODELED_PROFILE, FULL_ROW, KEY_ONLY, OP_TOPK, ModeledDevice, calibrate_profile
+from .device import DEFAULT_MODELED_PROFILE, FULL_ROW, KEY_ONLY, OP_PROBE, OP_TOPK, ModeledDevice, calibrate_profile
 from .errors import StrategyMismatchError
 from .gate import DEVICE, HOST, GateConfig, execute_gated, execute_path
 from .host import mix64
@@ -273,6 +273,10 @@ def calibrate_device_profile(device, ns: Sequence[int] = (100_000, 1_000_000, 4_
         device.probe(b, p)
         leds = sorted((device.probe(b, p).ledger for _ in range(repeats)), key=lambda lg: lg.total)
         probe_samples.append((2 * half, leds[len(leds) // 2]))
+    if len({n for n, _ in probe_samples}) >= 3:
+        # Probes return tens of MB, so their ledgers pin both link bandwidths;
+        # Top-K ledgers (a few hundred bytes back) then supply kernel_rate_topk.
+        return calibrate_profile(probe_samples, op=OP_PROBE, probe_samples=samples)
     return calibrate_profile(samples, op=OP_TOPK, probe_samples=probe_samples)
 
 
