@@ -110,6 +110,8 @@ int golp_host_free(void* ptr, uint64_t bytes);
 /* Page-lock a caller buffer in place (read-only) so that transfers of it skip
  * the staging copy; for columns reused across calls (registration is slow). */
 int golp_host_register(const void* ptr, uint64_t bytes);
+/* 1 when ptr is page-locked host memory the DMA engines can use directly. */
+int golp_host_is_pinned(const void* ptr);
 int golp_host_unregister(const void* ptr);
 
 /* ---- device-resident entry points (inputs already in HBM) ---------------------- */

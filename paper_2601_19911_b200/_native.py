@@ -77,6 +77,7 @@ SIGNATURES = {
     "golp_host_alloc": (_vp, [_u64]),
     "golp_host_free": (_int, [_vp, _u64]),
     "golp_host_register": (_int, [_vp, _u64]),
+    "golp_host_is_pinned": (_int, [_vp]),
     "golp_host_unregister": (_int, [_vp]),
     "golp_host_topk": (_int, [_vp, _vp, _u64, _u64, _vp, _int]),
     "golp_host_hash_build": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),

@@ -96,8 +96,9 @@ struct Ctx {
   std::vector<D2HPiece> d2h_q;  // FIFO (front = index d2h_head)
   size_t d2h_head = 0;
   bool d2h_direct = false;  // direct (pinned-destination) copies pending on s_d2h
-  std::vector<cudaEvent_t> chunk_ev;
-  uint64_t* mirror = nullptr;  // pinned copy of per-chunk pair totals
+  std::vector<cudaEvent_t> chunk_ev, h2d_ev;
+  uint64_t* mirror = nullptr;  // mapped pinned copy of per-chunk pair totals
+  uint64_t* mirror_dev = nullptr;
   size_t mirror_n = 0;
   void* pin_small = nullptr;  // samples, counters, small outputs
   size_t pin_small_bytes = 16u << 20;
@@ -280,18 +281,31 @@ int sync_ring() {
 
 int ensure_chunk_events(size_t n) {
   while (g.chunk_ev.size() < n) {
-    cudaEvent_t e;
+    cudaEvent_t e, f;
     CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&f, cudaEventDisableTiming));
     g.chunk_ev.push_back(e);
+    g.h2d_ev.push_back(f);
   }
   if (g.mirror_n < n + 1) {
     if (g.mirror) cudaFreeHost(g.mirror);
     g.mirror = nullptr;
     g.mirror_n = 0;
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&g.mirror), (n + 1) * 8, cudaHostAllocDefault));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&g.mirror), (n + 2) * 8, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g.mirror_dev), g.mirror, 0));
     g.mirror_n = n + 1;
   }
   return GOLP_OK;
+}
+
+// Publishes a device counter to mapped pinned host memory with a one-thread
+// kernel: a memcpy here would sit in the D2H copy queue ahead of the pair
+// downloads and block them (head-of-line) until its stream dependency clears.
+__global__ void publish_u64_kernel(volatile unsigned long long* host_dst, const unsigned long long* src,
+                                   volatile unsigned int* host_flag, const unsigned int* flag) {
+  *host_dst = *src;
+  if (host_flag) *host_flag = *flag;
+  __threadfence_system();
 }
 
 // ---- pinned result arena ---------------------------------------------------------
@@ -739,9 +753,12 @@ int golp_shutdown(void) {
   g.d2h_head = 0;
   g.d2h_direct = false;
   for (cudaEvent_t e : g.chunk_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : g.h2d_ev) cudaEventDestroy(e);
   g.chunk_ev.clear();
+  g.h2d_ev.clear();
   if (g.mirror) cudaFreeHost(g.mirror);
   g.mirror = nullptr;
+  g.mirror_dev = nullptr;
   g.mirror_n = 0;
   // the pinned result arena outlives shutdown: result arrays may still be alive
   for (auto& e : g.ev) {
@@ -848,6 +865,31 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
   g.kt.topk_candidates = 0;
 
   cudaEvent_t ev_chunk = g.ev[0];
+  const uint64_t per_chunk = std::max<uint64_t>(g.chunk / 8, 1);
+  if (n <= per_chunk) {
+    // One chunk: upload both columns, then the device-resident pipeline (the
+    // samples are drawn on the device; nothing to overlap with).
+    RET(stage_h2d(dk, keys, n * 8));
+    RET(stage_h2d(dr, rows, n * 4));
+    if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(n * (size_t)payload_bytes));
+    CK(cudaEventRecord(ev_chunk, g.s_h2d));
+    CK(cudaEventSynchronize(ev_chunk));
+    g.next_slot = 0;
+    for (bool& b : g.pin_busy) b = false;
+    const double t1 = wall_seconds();
+    CK(cudaStreamWaitEvent(s, ev_chunk, 0));
+    uint32_t* d_out = g.out_rows.as<uint32_t>();
+    RET(topk_device_impl(dk, dr, n, kk, d_out, nullptr, s));
+    const double t2 = wall_seconds();
+    uint32_t* hbuf = static_cast<uint32_t*>(g.pin_small);
+    CK(cudaMemcpyAsync(hbuf, d_out, kk * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::memcpy(out_rows, hbuf, kk * 4);
+    led->t_h2d = t1 - t0;
+    led->t_kernel = t2 - t1;
+    led->t_d2h = wall_seconds() - t2;
+    return GOLP_OK;
+  }
   if (!p.direct) {
     // Stratified samples gathered on the host (same strata as SrcSample).
     double* hs = static_cast<double*>(g.pin_small);
@@ -869,7 +911,6 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     RET(launch_select(make_args(SrcInput{ds, dsr}, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), s));
   }
   // Stream the columns chunk by chunk; filter each chunk as soon as it lands.
-  const uint64_t per_chunk = std::max<uint64_t>(g.chunk / 8, 1);
   for (uint64_t c0 = 0; c0 < n; c0 += per_chunk) {
     const uint64_t cn = std::min(per_chunk, n - c0);
     RET(stage_h2d(dk + c0, keys + c0, cn * 8));
@@ -963,15 +1004,22 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   CK(cudaMemsetAsync(g.totals.p, 0, (nchunks + 1) * 8, s));
   RET(ensure_chunk_events(nchunks));
   g.mirror[0] = 0;
+  // Pairs land in HBM and stream back through the D2H engine chunk by chunk.
+  // (A zero-copy variant -- the emit kernel storing pairs into the pinned arena
+  // over PCIe -- measured 3x slower at C2: 4-byte scattered stores make poor
+  // PCIe transactions.)
   uint64_t dcap = std::max<uint64_t>(g.pairs_p.bytes / 4, std::max<uint64_t>(np, 1024));
   CK(g.pairs_p.ensure(dcap * 4));
   CK(g.pairs_b.ensure(dcap * 4));
   dcap = std::min(g.pairs_p.bytes, g.pairs_b.bytes) / 4;
+  uint32_t* dev_p = g.pairs_p.as<uint32_t>();
+  uint32_t* dev_b = g.pairs_b.as<uint32_t>();
   unsigned long long* totals = g.totals.as<unsigned long long>();
   // Pairs of chunk c stream back (DMA + unpack into the caller's arrays) while
   // later chunks upload; a chunk is ready once its probe event has fired.
   uint64_t streamed = 0;     // chunks whose pairs are queued for D2H
   bool streaming = out_cap > 0;
+  const bool trace = std::getenv("GOLP_TRACE") != nullptr;
   auto stream_ready = [&](bool block) -> int {
     while (streaming && streamed < nchunks) {
       cudaEvent_t e = g.chunk_ev[streamed];
@@ -983,65 +1031,117 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
         CK(q);
       }
       const uint64_t lo = g.mirror[streamed], hi = g.mirror[streamed + 1];
+      if (trace) std::fprintf(stderr, "[golp] %.3f ms chunk %llu probed, pairs [%llu, %llu)\n", (wall_seconds() - t0) * 1e3,
+                              (unsigned long long)streamed, (unsigned long long)lo, (unsigned long long)hi);
       if (hi > out_cap || hi > dcap) {
         streaming = false;  // caller's arrays (or the device buffer) too small: copy_out path
         break;
       }
       if (hi > lo) {
-        RET(d2h_enqueue(out_probe_rows + lo, g.pairs_p.as<uint32_t>() + lo, (hi - lo) * 4));
-        RET(d2h_enqueue(out_build_rows + lo, g.pairs_b.as<uint32_t>() + lo, (hi - lo) * 4));
+        RET(d2h_enqueue(out_probe_rows + lo, dev_p + lo, (hi - lo) * 4));
+        RET(d2h_enqueue(out_build_rows + lo, dev_b + lo, (hi - lo) * 4));
       }
       ++streamed;
     }
     return d2h_poll();
   };
-  auto run_chunks = [&](bool with_h2d) -> int {
+  auto run_chunks = [&](bool with_h2d, uint32_t* op, uint32_t* ob, uint64_t cap_) -> int {
     for (uint64_t c = 0; c < nchunks; ++c) {
       const uint64_t c0 = c * per_chunk;
       const uint64_t cn = std::min(per_chunk, np - c0);
       if (with_h2d) {
+        // Keep at most two chunks of uploads in flight: copies are serviced in
+        // submission order, so pair downloads queued in between can overlap them.
+        if (c >= 2) {
+          while (true) {
+            const cudaError_t q = cudaEventQuery(g.h2d_ev[c - 2]);
+            if (q == cudaSuccess) break;
+            if (q != cudaErrorNotReady) CK(q);
+            RET(stream_ready(false));
+            std::this_thread::yield();
+          }
+        }
         RET(stage_h2d(dpk + c0, probe_keys + c0, cn * 8));
         RET(stage_h2d(dpr + c0, probe_rows + c0, cn * 4));
         if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(cn * (size_t)payload_bytes));
-        CK(cudaEventRecord(ev_chunk, g.s_h2d));
-        CK(cudaStreamWaitEvent(s, ev_chunk, 0));
+        CK(cudaEventRecord(g.h2d_ev[c], g.s_h2d));
+        CK(cudaStreamWaitEvent(s, g.h2d_ev[c], 0));
       }
-      RET(launch_probe(dpk + c0, dpr + c0, cn, g.pairs_p.as<uint32_t>(), g.pairs_b.as<uint32_t>(), dcap,
-                       totals + c, totals + c + 1, s));
-      if (with_h2d) {
-        CK(cudaMemcpyAsync(g.mirror + c + 1, totals + c + 1, 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaEventRecord(g.chunk_ev[c], s));
-        CK(cudaStreamWaitEvent(g.s_d2h, g.chunk_ev[c], 0));
-        RET(stream_ready(false));
-      }
+      RET(launch_probe(dpk + c0, dpr + c0, cn, op, ob, cap_, totals + c, totals + c + 1, s));
+      publish_u64_kernel<<<1, 1, 0, s>>>(reinterpret_cast<volatile unsigned long long*>(g.mirror_dev + c + 1),
+                                         totals + c + 1,
+                                         reinterpret_cast<volatile unsigned int*>(g.mirror_dev + nchunks + 1),
+                                         g.jflags.as<unsigned int>());
+      CKL();
+      ++g_launches;
+      CK(cudaEventRecord(g.chunk_ev[c], s));
+      if (with_h2d) RET(stream_ready(false));
     }
     return GOLP_OK;
   };
-  RET(run_chunks(true));
+  g.mirror[nchunks + 1] = 0;
+  RET(run_chunks(true, dev_p, dev_b, dcap));
+  if (trace) std::fprintf(stderr, "[golp] %.3f ms all chunks queued\n", (wall_seconds() - t0) * 1e3);
   CK(cudaEventRecord(ev_chunk, g.s_h2d));
-  CK(cudaEventSynchronize(ev_chunk));
+  // Wait for the last upload while still handing finished chunks' pairs to the
+  // D2H engine, so downloads overlap the remaining uploads.
+  while (true) {
+    const cudaError_t q = cudaEventQuery(ev_chunk);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) CK(q);
+    RET(stream_ready(false));
+    std::this_thread::yield();
+  }
   g.next_slot = 0;
   for (bool& b : g.pin_busy) b = false;
   const double t1 = wall_seconds();
+  if (trace) std::fprintf(stderr, "[golp] %.3f ms uploads done\n", (t1 - t0) * 1e3);
+  auto finished_total = [&](uint64_t* m_out) -> int {  // totals via the mapped mirror (no copy engine)
+    if (nchunks) {
+      CK(cudaEventSynchronize(g.chunk_ev[nchunks - 1]));
+      *m_out = g.mirror[nchunks];
+      if ((uint32_t)g.mirror[nchunks + 1] != 0) {
+        set_error("a build key occurs more than 2^24-1 times; the packed probe entry cannot describe it");
+        return GOLP_ERR_CAPACITY;
+      }
+    } else {
+      CK(cudaStreamSynchronize(s));
+      *m_out = 0;
+    }
+    return GOLP_OK;
+  };
+  while (streaming && streamed < nchunks) {  // keep streaming while the last chunks finish
+    const cudaError_t q = cudaEventQuery(g.chunk_ev[nchunks - 1]);
+    if (q != cudaErrorNotReady) {
+      CK(q);
+      break;
+    }
+    RET(stream_ready(false));
+    std::this_thread::yield();
+  }
   uint64_t m = 0;
-  RET(read_probe_total(totals + nchunks, &m, s));
+  RET(finished_total(&m));
   const double t2 = wall_seconds();
-  if (m > dcap) {  // rare: more pairs than probes; grow and re-probe the resident input
+  if (trace) std::fprintf(stderr, "[golp] %.3f ms last chunk probed, M=%llu\n", (t2 - t0) * 1e3, (unsigned long long)m);
+  if (m > dcap) {  // rare: more pairs than the output capacity; re-probe the resident input into HBM
     streaming = false;
     RET(d2h_flush());
     CK(g.pairs_p.ensure(m * 4));
     CK(g.pairs_b.ensure(m * 4));
     dcap = std::min(g.pairs_p.bytes, g.pairs_b.bytes) / 4;
     CK(cudaMemsetAsync(g.totals.p, 0, (nchunks + 1) * 8, s));
-    RET(run_chunks(false));
-    RET(read_probe_total(totals + nchunks, &m, s));
+    RET(run_chunks(false, g.pairs_p.as<uint32_t>(), g.pairs_b.as<uint32_t>(), dcap));
+    RET(finished_total(&m));
+    dev_p = g.pairs_p.as<uint32_t>();
+    dev_b = g.pairs_b.as<uint32_t>();
   }
   RET(stream_ready(true));
   RET(d2h_flush());
   const double t3 = wall_seconds();
+  if (trace) std::fprintf(stderr, "[golp] %.3f ms pairs landed\n", (t3 - t0) * 1e3);
   *out_matches = m;
   g.last_m = m;
-  g.last_probe_valid = true;
+  g.last_probe_valid = true;  // copy_out reads the device pair buffers
   const bool delivered = streaming && m <= out_cap && streamed == nchunks;
   led->t_h2d = t1 - t0;
   led->t_kernel = t2 - t1;
@@ -1090,6 +1190,8 @@ int golp_host_free(void* p, uint64_t bytes) {
   if (bytes == 0) bytes = 1;
   return munmap(p, bytes) == 0 ? GOLP_OK : GOLP_ERR_INVALID;
 }
+
+int golp_host_is_pinned(const void* p) { return is_pinned(p) ? 1 : 0; }
 
 // Page-lock a caller buffer in place (read-only) so repeated transfers of it skip
 // the staging copy. Slow (~5 GB/s): worth it only for buffers reused across calls.
