@@ -114,6 +114,8 @@ struct Ctx {
   uint64_t last_m = 0;
   bool last_probe_valid = false;
 
+  char* status_host = nullptr;  // mapped pinned words: select status + candidate count
+  char* status_dev = nullptr;
   bool prof = false;
   bool build_timed = false;
   golp_kernel_times kt{};
@@ -413,6 +415,17 @@ template <class Src>
 int launch_select(const SelectArgs<Src>& a, cudaStream_t s) {
   static int blocks = 0;
   const size_t smem = (size_t)kSortTile * (sizeof(uint64_t) + sizeof(uint32_t));
+  if (!a.use_cand_count && a.n <= kSortTile) {  // one block, shared memory only: plain launch
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(select_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    select_kernel<Src><<<1, kSelThreads, smem, s>>>(a);
+    CKL();
+    ++g_launches;
+    return GOLP_OK;
+  }
   if (!blocks) {
     CK(cudaFuncSetAttribute(select_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;
@@ -444,6 +457,8 @@ SelectArgs<Src> make_args(Src src, uint64_t n, uint64_t need, int mode, int c, u
   a.w_lo = g.w_lo.as<uint32_t>();
   a.out_rows = out_rows;
   a.out_hi = out_hi;
+  a.host_status = nullptr;
+  a.host_count = nullptr;
   return a;
 }
 
@@ -479,19 +494,32 @@ double prof_ms(int a, int b) {
   return (double)ms;
 }
 
-// Reads ctl(1) status / candidate count after a sampled run (synchronises s).
-int read_topk_status(cudaStream_t s, int* bad, uint64_t* cands) {
-  struct Tail {
-    unsigned long long cand_count;
-    int status;
-  };
-  Tail* t = static_cast<Tail*>(g.pin_small);
-  CK(cudaMemcpyAsync(&t->cand_count, &ctl(1)->cand_count, 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(&t->status, &ctl(1)->status, 4, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  *bad = t->status != 0;
-  *cands = t->cand_count;
+// Status / candidate count of a sampled run: the select kernel stores them into
+// mapped pinned words, so one stream sync replaces a D2H copy + sync.
+int ensure_status_words() {
+  if (!g.status_host) {
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&g.status_host), 64, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g.status_dev), g.status_host, 0));
+  }
   return GOLP_OK;
+}
+
+int read_topk_status(cudaStream_t s, int* bad, uint64_t* cands) {
+  CK(cudaStreamSynchronize(s));
+  *bad = *reinterpret_cast<volatile int*>(g.status_host) != 0;
+  *cands = *reinterpret_cast<volatile unsigned long long*>(g.status_host + 8);
+  return GOLP_OK;
+}
+
+SelectArgs<SrcCand> cand_args(uint64_t kk, uint64_t cap, uint32_t* out_rows, uint64_t* out_hi) {
+  SelectArgs<SrcCand> a = make_args(SrcCand{g.cand_hi.as<uint64_t>(), g.cand_lo.as<uint32_t>()}, 0, kk, kModeFull, 1,
+                                    out_rows, out_hi);
+  a.use_cand_count = 1;
+  a.cap = cap;
+  *reinterpret_cast<volatile int*>(g.status_host) = 0;
+  a.host_status = reinterpret_cast<int*>(g.status_dev);
+  a.host_count = reinterpret_cast<unsigned long long*>(g.status_dev + 8);
+  return a;
 }
 
 // Exact fallback: radix select straight over the device-resident input.
@@ -520,15 +548,12 @@ int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint6
     CK(cudaStreamSynchronize(s));
   } else {
     CK(cudaMemsetAsync(ctl(0), 0, sizeof(SelectCtl) * 2, s));
-    RET(launch_select(make_args(SrcSample{keys, rows, n, p.s}, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), s));
+    RET(launch_select(make_args(SrcSample{keys, rows, n, (uint32_t)std::max<uint64_t>(1, n / p.s)}, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), s));
     prof_record(1, s);
     RET(launch_filter(keys, rows, n, p.cap, s));
     prof_record(2, s);
-    SelectArgs<SrcCand> a = make_args(SrcCand{g.cand_hi.as<uint64_t>(), g.cand_lo.as<uint32_t>()}, 0, kk,
-                                      kModeFull, 1, out_rows, out_hi);
-    a.use_cand_count = 1;
-    a.cap = p.cap;
-    RET(launch_select(a, s));
+    RET(ensure_status_words());
+    RET(launch_select(cand_args(kk, p.cap, out_rows, out_hi), s));
     prof_record(3, s);
     int bad = 0;
     uint64_t cands = 0;
@@ -743,6 +768,8 @@ int golp_shutdown(void) {
   }
   if (g.pin_small) cudaFreeHost(g.pin_small);
   g.pin_small = nullptr;
+  if (g.status_host) cudaFreeHost(g.status_host);
+  g.status_host = g.status_dev = nullptr;
   for (int i = 0; i < kD2HSlots; ++i) {
     if (g.dpin[i]) cudaFreeHost(g.dpin[i]);
     if (g.dpin_ev[i]) cudaEventDestroy(g.dpin_ev[i]);
@@ -894,10 +921,9 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     // Stratified samples gathered on the host (same strata as SrcSample).
     double* hs = static_cast<double*>(g.pin_small);
     uint32_t* hr = reinterpret_cast<uint32_t*>(hs + p.s);
+    const uint32_t w = (uint32_t)std::max<uint64_t>(1, n / p.s);
     for (uint64_t i = 0; i < p.s; ++i) {
-      const uint64_t lo = (i * n) / p.s, hi = ((i + 1) * n) / p.s;
-      const uint64_t w = hi > lo ? hi - lo : 1;
-      uint64_t pos = lo + (hash32((uint32_t)i * 2654435761u + 12345u) % w);
+      uint64_t pos = i * w + (hash32((uint32_t)i * 2654435761u + 12345u) % w);
       if (pos >= n) pos = n - 1;
       hs[i] = keys[pos];
       hr[i] = rows[pos];
@@ -933,11 +959,8 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     RET(topk_direct(dk, dr, n, kk, d_out, nullptr, s));
     CK(cudaStreamSynchronize(s));
   } else {
-    SelectArgs<SrcCand> a = make_args(SrcCand{g.cand_hi.as<uint64_t>(), g.cand_lo.as<uint32_t>()}, 0, kk,
-                                      kModeFull, 1, d_out, nullptr);
-    a.use_cand_count = 1;
-    a.cap = p.cap;
-    RET(launch_select(a, s));
+    RET(ensure_status_words());
+    RET(launch_select(cand_args(kk, p.cap, d_out, nullptr), s));
     int bad = 0;
     uint64_t cands = 0;
     RET(read_topk_status(s, &bad, &cands));

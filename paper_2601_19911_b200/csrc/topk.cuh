@@ -67,17 +67,15 @@ struct SrcPairs {  // encoded keys + plain row ids (all-gathered local Top-K res
 };
 
 // S stratified samples of an n-item column: sample i comes from stratum
-// [i*n/S, (i+1)*n/S) at a hashed offset, so periodic layouts cannot alias.
+// [i*w, (i+1)*w) (w = n / S) at a hashed offset, so periodic layouts cannot
+// alias. 32-bit arithmetic only (64-bit division costs ~100 instructions).
 struct SrcSample {
   const double* keys;
   const uint32_t* rows;
   uint64_t n;
-  uint64_t s;
+  uint32_t w;  // stratum width, >= 1
   __device__ __forceinline__ uint64_t pos(uint64_t i) const {
-    const uint64_t lo_ = (i * n) / s;
-    const uint64_t hi_ = ((i + 1) * n) / s;
-    const uint64_t w = hi_ > lo_ ? hi_ - lo_ : 1;
-    uint64_t p = lo_ + (hash32((uint32_t)i * 2654435761u + 12345u) % w);
+    const uint64_t p = i * w + (hash32((uint32_t)i * 2654435761u + 12345u) % w);
     return p < n ? p : n - 1;
   }
   __device__ __forceinline__ uint64_t hi(uint64_t i) const { return ord_key(__ldg(keys + pos(i))); }
@@ -97,6 +95,8 @@ struct SelectArgs {
   uint32_t* w_lo;
   uint32_t* out_rows;  // need entries, best first
   uint64_t* out_hi;    // optional: encoded keys of the winners (for merges)
+  int* host_status;    // optional mapped host word: 1 when the candidate set was unusable
+  unsigned long long* host_count;  // optional mapped host word: candidate count
 };
 
 // Compare the top `bits` bits of (h, l) against the prefix: -1, 0, +1.
@@ -113,9 +113,90 @@ __device__ __forceinline__ int prefix_cmp(uint64_t h, uint32_t l, uint64_t ph, u
   return a > b ? 1 : (a < b ? -1 : 0);
 }
 
+
+// ---- single-block selection in shared memory -------------------------------------
+// MSB radix select of the `need` best of n items held in shared memory (8-bit
+// digits over the 96-bit composite, smem histogram, one warp resolves the digit).
+// Leaves the resolved prefix in *pre_hi/*pre_lo/*bits and the count still to
+// take from the prefix bucket in *rem (same contract as the grid engine).
+// With `coarse`, stops as soon as the prefix bucket holds at most 2*need items:
+// everything >= the prefix is still a superset of the best `need` (threshold use).
+__device__ void block_radix_select(const uint64_t* s_hi, const uint32_t* s_lo, uint32_t n, uint64_t need,
+                                   unsigned* s_hist, uint64_t* sh_pre_hi, uint32_t* sh_pre_lo, int* sh_bits,
+                                   unsigned long long* sh_rem, int* sh_done, bool coarse = false) {
+  if (threadIdx.x == 0) {
+    *sh_pre_hi = 0;
+    *sh_pre_lo = 0;
+    *sh_bits = 0;
+    *sh_rem = need;
+    *sh_done = 0;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 12; ++pass) {
+    const uint64_t pre_hi = *sh_pre_hi;
+    const uint32_t pre_lo = *sh_pre_lo;
+    const int bits = *sh_bits;
+    const unsigned long long rem = *sh_rem;
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) s_hist[t] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t h = s_hi[i];
+      unsigned d;
+      if (bits < 64) {
+        if (bits > 0 && (h >> (64 - bits)) != (pre_hi >> (64 - bits))) continue;
+        d = (unsigned)(h >> (56 - bits)) & 255u;
+      } else {
+        if (h != pre_hi) continue;
+        const uint32_t l = s_lo[i];
+        if (bits > 64 && (l >> (96 - bits)) != (pre_lo >> (96 - bits))) continue;
+        d = (l >> (24 - (bits - 64))) & 255u;
+      }
+      atomicAdd(&s_hist[d], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      unsigned c8[8];
+      unsigned long long lsum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        c8[q] = s_hist[255 - 8 * lane - q];
+        lsum += c8[q];
+      }
+      unsigned long long incl = lsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const unsigned long long excl = incl - lsum;
+      if (excl < rem && incl >= rem) {
+        unsigned long long cum = excl;
+        int b = -1;
+        unsigned cb = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (b < 0 && cum + c8[q] >= rem) { b = 255 - 8 * lane - q; cb = c8[q]; }
+          else if (b < 0) cum += c8[q];
+        }
+        uint64_t ph = pre_hi;
+        uint32_t pl = pre_lo;
+        if (bits < 64) ph |= (uint64_t)b << (56 - bits);
+        else pl |= (uint32_t)b << (24 - (bits - 64));
+        *sh_pre_hi = ph;
+        *sh_pre_lo = pl;
+        *sh_bits = bits + 8;
+        *sh_rem = rem - cum;
+        *sh_done = (rem - cum == cb) || (bits + 8 >= 96) || (coarse && cb <= 2 * need);
+      }
+    }
+    __syncthreads();
+    if (*sh_done) break;
+  }
+}
+
 template <class Src>
 __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs<Src> a) {
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* s_hi = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* s_lo = reinterpret_cast<uint32_t*>(s_hi + kSortTile);
@@ -130,8 +211,13 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs<Src> a) 
   uint64_t n = a.n;
   if (a.use_cand_count) {
     const unsigned long long c = *(volatile unsigned long long*)&a.ctl->cand_count;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.host_count) *(volatile unsigned long long*)a.host_count = c;
     if (c > a.cap || c < a.need) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->status = 1;
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ctl->status = 1;
+        if (a.host_status) *(volatile int*)a.host_status = 1;
+        __threadfence_system();
+      }
       return;  // uniform across the grid: no barrier is ever reached
     }
     n = c;
@@ -140,14 +226,67 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs<Src> a) 
   const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
 
-  // Small lists: one block sorts everything and emits the best `need`.
-  if (a.mode == kModeFull && n <= kSortTile) {
+  // Small lists: one block, all in shared memory. Threshold mode resolves the
+  // need-th best by a smem radix select; full mode selects the best `need` the
+  // same way when that beats sorting everything, then sorts only those.
+  if (n <= kSortTile) {
     if (blockIdx.x != 0) return;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
       s_hi[i] = src.hi(i);
       s_lo[i] = src.lo(i);
     }
     __syncthreads();
+    if (a.mode == kModeThreshold || (need * 4 <= n && n > 1024)) {
+      block_radix_select(s_hi, s_lo, (uint32_t)n, need, s_hist, &sh_pre_hi, &sh_pre_lo, &sh_bits, &sh_rem, &sh_done,
+                         a.mode == kModeThreshold);
+      const uint64_t ph = sh_pre_hi;
+      const uint32_t pl = sh_pre_lo;
+      const int bits = sh_bits;
+      const unsigned long long rem = sh_rem;
+      if (a.mode == kModeThreshold) {
+        if (threadIdx.x == 0) {
+          a.ctl->thr_key = key_from_ord(ph);
+          a.ctl->thr_row = ~pl;
+          a.ctl->res_hi = ph;
+          a.ctl->res_lo = pl;
+          a.ctl->res_bits = bits;
+        }
+        return;
+      }
+      // collect the winners (held in registers while the list is read), then
+      // rewrite them to the front of the smem list and sort just them
+      uint64_t* w_hi = s_hi;
+      uint32_t* w_lo = s_lo;
+      __shared__ unsigned s_cnt, s_eq;
+      if (threadIdx.x == 0) { s_cnt = 0; s_eq = 0; }
+      __syncthreads();
+      uint64_t keep_hi[kSortTile / kSelThreads];
+      uint32_t keep_lo[kSortTile / kSelThreads];
+      unsigned nk = 0;
+      for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t h = s_hi[i];
+        const uint32_t l = s_lo[i];
+        const int c = prefix_cmp(h, l, ph, pl, bits);
+        if (c > 0 || (c == 0 && (bits < 96 || atomicAdd(&s_eq, 1u) < rem))) {
+          keep_hi[nk] = h;
+          keep_lo[nk] = l;
+          ++nk;
+        }
+      }
+      __syncthreads();  // all reads of s_hi/s_lo done before the winners overwrite them
+      for (unsigned q = 0; q < nk; ++q) {
+        const unsigned slot = atomicAdd(&s_cnt, 1u);
+        w_hi[slot] = keep_hi[q];
+        w_lo[slot] = keep_lo[q];
+      }
+      __syncthreads();
+      block_sort_desc(w_hi, w_lo, (uint32_t)need);
+      for (uint32_t i = threadIdx.x; i < need; i += blockDim.x) {
+        a.out_rows[i] = ~w_lo[i];
+        if (a.out_hi) a.out_hi[i] = w_hi[i];
+      }
+      return;
+    }
     block_sort_desc(s_hi, s_lo, (uint32_t)n);
     for (uint32_t i = threadIdx.x; i < need; i += blockDim.x) {
       a.out_rows[i] = ~s_lo[i];
@@ -157,6 +296,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs<Src> a) 
   }
 
   // ---- MSB radix select on the 96-bit composite, 8-bit digits ----------------
+  // (grid-wide from here on: only reached under a cooperative launch)
+  cg::grid_group grid = cg::this_grid();
   uint64_t pre_hi = 0;
   uint32_t pre_lo = 0;
   int bits = 0;

@@ -238,6 +238,54 @@ __global__ void r6(const double* keys, const uint32_t* rows, const ulonglong2* t
   }
 }
 
+// rung 7: cooperative 4-lane lookups on 128-byte buckets of 8 slots (one line):
+// lane q of a group loads sector q (2 slots); one wavefront serves 8 slots.
+// Items: lane l owns elements j=0..W-1 (blocked); at step (j, b) group g probes
+// the item of lane b*8+g, element j. Count hits.
+template <int W>
+__global__ void r7(const double* keys, const ulonglong2* t, uint64_t nbuckets_mask, uint64_t n,
+                   unsigned long long* out) {
+  unsigned long long acc = 0;
+  const unsigned lane = threadIdx.x & 31, grp = lane >> 2, q = lane & 3;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = (tid - lane) * W; i0 < n; i0 += st * W) {
+    const uint64_t i = i0 + lane * W;
+    uint64_t b[W];
+    uint32_t bk[W];
+#pragma unroll
+    for (int j = 0; j < W; j += 2) {
+      double2 k = __ldg(reinterpret_cast<const double2*>(keys + i + j));
+      b[j] = __double_as_longlong(k.x); b[j + 1] = __double_as_longlong(k.y);
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) bk[j] = (uint32_t)(mix64(b[j]) & nbuckets_mask);
+    unsigned hit = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      ulonglong4 v[4];
+      uint64_t kb[4];
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) {
+        const unsigned src = bb * 8 + grp;
+        kb[bb] = __shfl_sync(~0u, b[j], src);
+        const uint32_t buck = __shfl_sync(~0u, bk[j], src);
+        v[bb] = ldg_pair(t + (uint64_t)buck * 8 + q * 2);
+      }
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) {
+        const bool m = v[bb].x == kb[bb] || v[bb].z == kb[bb];
+        const unsigned bal = __ballot_sync(~0u, m);
+        const bool found = (bal >> (grp * 4)) & 0xF;
+        // owner lane of this item is bb*8+grp; lanes l with l>>3 == bb read group (l&7)
+        const unsigned fl = __shfl_sync(~0u, (unsigned)found, (lane & 7) * 4);
+        if ((lane >> 3) == (unsigned)bb && fl) hit |= 1u << j;
+      }
+    }
+    acc += __popc(hit);
+  }
+  if (acc == 0x123456) *out = acc;
+}
+
 int main() {
   const uint64_t nb = 1000000, np = 10000000, cap = 1 << 21, mask = cap - 1;
   std::mt19937_64 rng(1);
@@ -291,6 +339,34 @@ int main() {
     run(nm, [&] { r4<4><<<grid, 256>>>(dk, dr, dt, mask, np, sp, so, sc, wc); });
     snprintf(nm, 96, "r6 + smem-staged stores W4 grid %dx256", grid);
     run(nm, [&] { r6<4><<<grid, 256>>>(dk, dr, dt, mask, np, sp, so, sc, wc); });
+  }
+  // rung 7 on an 8-slot bucket table (same 2^21 slots: 2^18 buckets of 128 B)
+  {
+    const uint64_t nbk = cap / 8, bm = nbk - 1;
+    std::vector<ulonglong2> t8(cap, ulonglong2{kEmpty, 0});
+    for (double k : bk) {
+      uint64_t b; memcpy(&b, &k, 8);
+      uint64_t bi = mix64(b) & bm;
+      bool done = false;
+      while (!done) {
+        for (int s2 = 0; s2 < 8; ++s2) {
+          ulonglong2& sl = t8[bi * 8 + s2];
+          if (sl.x == b) { done = true; break; }
+          if (sl.x == kEmpty) { sl.x = b; sl.y = 1ull << 32; done = true; break; }
+        }
+        bi = (bi + 1) & bm;
+      }
+    }
+    ulonglong2* d8; CK(cudaMalloc(&d8, cap * 16));
+    CK(cudaMemcpy(d8, t8.data(), cap * 16, cudaMemcpyHostToDevice));
+    for (int bpsm : {4, 8}) {
+      char nm[96];
+      snprintf(nm, 96, "r7 coop-4 buckets of 8, W4 grid %dx256", sms * bpsm);
+      run(nm, [&] { r7<4><<<sms * bpsm, 256>>>(dk, d8, bm, np, out); });
+      snprintf(nm, 96, "r7 coop-4 buckets of 8, W2 grid %dx256", sms * bpsm);
+      run(nm, [&] { r7<2><<<sms * bpsm, 256>>>(dk, d8, bm, np, out); });
+    }
+    cudaFree(d8);
   }
   // lower load factors (same keys, bigger tables)
   for (uint64_t c2 : {uint64_t(1) << 22, uint64_t(1) << 23}) {
