@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <sys/mman.h>
+#include <unistd.h>
 
 #include <map>
 
@@ -313,9 +314,19 @@ __global__ void publish_u64_kernel(volatile unsigned long long* host_dst, const 
 // ---- pinned result arena ---------------------------------------------------------
 // Result arrays handed to Python live here: page-locked, so pairs DMA straight
 // into them. First-fit over 2 MB-granular blocks, coalescing frees; regions are
-// added on demand up to kArenaMax, beyond that golp_host_alloc falls back to mmap.
+// added on demand up to arena_max(), beyond that golp_host_alloc falls back to mmap.
 constexpr size_t kArenaRegion = size_t(256) << 20;
-constexpr size_t kArenaMax = size_t(4) << 30;
+// Cap on page-locked result memory: a quarter of host RAM (pinned pages cannot
+// be swapped or reclaimed), at least 4 GiB.
+size_t arena_max() {
+  static size_t cap = 0;
+  if (!cap) {
+    const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGESIZE);
+    const size_t ram = (pages > 0 && psz > 0) ? (size_t)pages * (size_t)psz : (size_t(16) << 30);
+    cap = std::max(ram / 4, size_t(4) << 30);
+  }
+  return cap;
+}
 constexpr size_t kArenaGrain = size_t(2) << 20;
 struct ArenaRegion {
   char* base;
@@ -344,7 +355,7 @@ void* arena_alloc(size_t bytes) {
       }
     }
     const size_t want = std::max(kArenaRegion, len);
-    if (g_arena_total + want > kArenaMax || !g.ready) return nullptr;
+    if (g_arena_total + want > arena_max() || !g.ready) return nullptr;
     void* base = nullptr;
     if (cudaHostAlloc(&base, want, cudaHostAllocDefault) != cudaSuccess) {
       cudaGetLastError();
