@@ -134,6 +134,13 @@ int golp_join_probe_device(const double* d_probe_keys, const uint32_t* d_probe_r
                            uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
                            uint64_t* out_matches, void* stream);
 
+/* Asynchronous probe: enqueues the probe on `stream` and writes M to the device
+ * word d_out_matches; pairs beyond cap are dropped (the caller compares M with
+ * cap after synchronizing and re-probes with a larger buffer if needed). */
+int golp_join_probe_device_async(const double* d_probe_keys, const uint32_t* d_probe_rows, uint64_t np,
+                                 uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
+                                 uint64_t* d_out_matches, void* stream);
+
 /* ---- classical host engine (the gate's HOST path, gate.py:193-194,209-210) ------ */
 /* Multi-threaded CPU Top-K with host_topk's exact output (host.py:133-144). */
 int golp_host_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, uint32_t* out_rows,

@@ -74,6 +74,7 @@ SIGNATURES = {
     "golp_topk_merge_device": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
     "golp_join_build_device": (_int, [_vp, _vp, _u64, _vp]),
     "golp_join_probe_device": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, C.POINTER(_u64), _vp]),
+    "golp_join_probe_device_async": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
     "golp_host_alloc": (_vp, [_u64]),
     "golp_host_free": (_int, [_vp, _u64]),
     "golp_host_register": (_int, [_vp, _u64]),

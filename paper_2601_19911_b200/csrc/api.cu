@@ -107,8 +107,8 @@ struct Ctx {
   cudaEvent_t ev[8] = {};
 
   DevBuf ctl, cand_hi, cand_lo, w_hi, w_lo, out_rows, out_hi, samples;
-  DevBuf table, bslot, brank, csr_pos, csr_row, big_list, jcount, wcount, partial, totals, totals2;
-  DevBuf sc_entry, jflags;
+  DevBuf table, rows_arr, ovf, big_list, jcount, wcount, partial, totals, totals2;
+  DevBuf sc_prow, sc_off, sc_cnt, jflags;
   DevBuf pairs_p, pairs_b;
   DevBuf in_keys, in_rows, in_bkeys, in_brows, in_payload;
   uint64_t jcap = 0, jmask = 0, jnb = 0;
@@ -119,6 +119,7 @@ struct Ctx {
   char* status_dev = nullptr;
   bool prof = false;
   bool build_timed = false;
+  bool probe_timed = false;
   golp_kernel_times kt{};
 };
 
@@ -595,48 +596,46 @@ int grid_for(uint64_t n, int threads, int per_sm) {
 int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cudaStream_t s) {
   uint64_t cap = 1024;
   while (cap < 2 * nb && cap < (1ull << 32)) cap <<= 1;
-  if (cap < 2 * nb) {
-    set_error("join build side too large for 32-bit slot indices");
+  if (cap < 2 * nb || cap * kInline + nb > (1ull << 32)) {
+    set_error("join build side too large for 32-bit slot / row indices");
     return GOLP_ERR_CAPACITY;
   }
-  CK(g.table.ensure(cap * sizeof(Slot)));
   const uint64_t nbb = std::max<uint64_t>(nb, 1);
-  CK(g.bslot.ensure(nbb * 4));
-  CK(g.brank.ensure(nbb * 4));
-  CK(g.csr_pos.ensure(nbb * 4));
-  CK(g.csr_row.ensure(nbb * 4));
-  CK(g.big_list.ensure((nbb / (kSmallGroup + 1) + 1) * 4));
-  CK(g.jcount.ensure(16));
+  CK(g.table.ensure(cap * sizeof(Slot)));
+  CK(g.rows_arr.ensure((cap * kInline + nbb) * 4));
+  CK(g.ovf.ensure(nbb * 12));
+  CK(g.big_list.ensure((nbb / (kInline + 1) * 2 + 2) * 4));
+  CK(g.jcount.ensure(32));
+  CK(g.jflags.ensure(4));
   g.jcap = cap;
   g.jmask = cap - 1;
   g.jnb = nb;
   Slot* table = g.table.as<Slot>();
+  GroupArrays ga;
+  ga.rows = g.rows_arr.as<uint32_t>();
+  ga.ovf_slot = g.ovf.as<uint32_t>();
+  ga.ovf_rank = ga.ovf_slot + nbb;
+  ga.ovf_pos = ga.ovf_rank + nbb;
+  ga.counters = g.jcount.as<unsigned long long>();
+  ga.big_list = g.big_list.as<uint32_t>();
   prof_record(4, s);
   join_init_table_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap);
   CKL();
   ++g_launches;
-  CK(cudaMemsetAsync(g.jcount.p, 0, 16, s));
-  CK(g.jflags.ensure(4));
+  CK(cudaMemsetAsync(g.jcount.p, 0, 32, s));
   CK(cudaMemsetAsync(g.jflags.p, 0, 4, s));
   if (nb == 0) {
     prof_record(5, s);
     return GOLP_OK;
   }
-  unsigned long long* cursor = g.jcount.as<unsigned long long>();
-  unsigned int* big_count = reinterpret_cast<unsigned int*>(cursor + 1);
   const int gb = grid_for((nb + kBuildItems - 1) / kBuildItems, kBuildThreads, 8);
-  join_insert_kernel<<<gb, kBuildThreads, 0, s>>>(bkeys, nb, table, g.jmask, g.bslot.as<uint32_t>(),
-                                                  g.brank.as<uint32_t>());
+  join_insert_kernel<<<gb, kBuildThreads, 0, s>>>(bkeys, nb, table, g.jmask, ga);
   CKL();
-  join_offsets_kernel<<<gb, kBuildThreads, 0, s>>>(nb, table, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>(), brows,
-                                                   cursor, g.big_list.as<uint32_t>(), big_count);
+  join_finalize_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, brows, ga, cap * kInline);
   CKL();
-  join_fill_kernel<<<gb, kBuildThreads, 0, s>>>(nb, table, g.bslot.as<uint32_t>(), g.brank.as<uint32_t>(),
-                                                g.csr_pos.as<uint32_t>());
+  join_overflow_kernel<<<g.sms * 2, 256, 0, s>>>(table, ga);
   CKL();
-  join_small_groups_kernel<<<grid_for(nb, 256, 8), 256, 0, s>>>(nb, table, g.bslot.as<uint32_t>(),
-                                                                g.brank.as<uint32_t>(), g.csr_pos.as<uint32_t>(),
-                                                                brows, g.csr_row.as<uint32_t>());
+  join_group_sort_kernel<<<g.sms, 128, 0, s>>>(table, ga, brows);
   CKL();
   static bool attr = false;
   const size_t smem = kGroupTile * sizeof(uint32_t);
@@ -644,8 +643,7 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
     CK(cudaFuncSetAttribute(join_big_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  join_big_groups_kernel<<<g.sms, 1024, smem, s>>>(table, g.big_list.as<uint32_t>(), big_count,
-                                                   g.csr_pos.as<uint32_t>(), brows, g.csr_row.as<uint32_t>());
+  join_big_groups_kernel<<<g.sms, 1024, smem, s>>>(table, ga, brows);
   CKL();
   g_launches += 5;
   prof_record(5, s);
@@ -661,37 +659,43 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
     CK(cudaMemcpyAsync(total_out, base_in, 8, cudaMemcpyDeviceToDevice, s));
     return GOLP_OK;
   }
-  constexpr uint64_t kSub = 1ull << 27;  // probes per sub-chunk (scratch <= 1 GiB)
+  constexpr uint64_t kSub = 1ull << 27;  // probes per sub-chunk (scratch <= 1.5 GiB)
   const uint64_t sub = std::min(np, kSub);
   const uint64_t nwt_max = (sub + kWarpTile - 1) / kWarpTile;
-  CK(g.sc_entry.ensure(nwt_max * kWarpTile * 8));
-  CK(g.wcount.ensure(nwt_max * 8));
+  const uint64_t nwarps_max = (uint64_t)g.sms * GOLP_PROBE_MINB * kProbeWarps;
+  CK(g.sc_prow.ensure(nwt_max * kWarpTile * 4));
+  CK(g.sc_off.ensure(nwt_max * kWarpTile * 4));
+  CK(g.sc_cnt.ensure(nwt_max * kWarpTile * 4));
+  CK(g.wcount.ensure(std::max(nwt_max, nwarps_max) * 8));
   CK(g.totals2.ensure(16));
   MatchScratch sc;
-  sc.entry = g.sc_entry.as<uint2>();
-  sc.nmatch = g.wcount.as<uint32_t>();
-  sc.npairs = sc.nmatch + nwt_max;
+  sc.prow = g.sc_prow.as<uint32_t>();
+  sc.off = g.sc_off.as<uint32_t>();
+  sc.cnt = g.sc_cnt.as<uint32_t>();
   unsigned long long* tmp = g.totals2.as<unsigned long long>();
   for (uint64_t c0 = 0; c0 < np; c0 += kSub) {
     const uint64_t cn = std::min(kSub, np - c0);
     const uint64_t nwt = (cn + kWarpTile - 1) / kWarpTile;
-    uint64_t blocks = (uint64_t)g.sms * GOLP_PROBE_MINB;
-    blocks = std::max<uint64_t>(blocks, (nwt + kMaxTilesPerBlock - 1) / kMaxTilesPerBlock);
-    blocks = std::min<uint64_t>(blocks, nwt);
-    const uint64_t per_block = (nwt + blocks - 1) / blocks;
-    blocks = (nwt + per_block - 1) / per_block;
+    // one contiguous run of tiles per warp; enough warps to fill the GPU
+    const uint64_t want_warps = std::min<uint64_t>(nwarps_max, nwt);
+    const uint64_t per_warp = (nwt + want_warps - 1) / want_warps;
+    const uint64_t warps = (nwt + per_warp - 1) / per_warp;
+    const uint64_t blocks = (warps + kProbeWarps - 1) / kProbeWarps;
+    sc.wentries = g.wcount.as<uint32_t>();
+    sc.wpairs = sc.wentries + blocks * kProbeWarps;
     CK(g.partial.ensure(blocks * 8));
     unsigned long long* part = g.partial.as<unsigned long long>();
-    join_match_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(pkeys + c0, cn, g.table.as<Slot>(), g.jmask, sc, nwt,
-                                                                 per_block, part, g.jflags.as<unsigned int>());
+    join_match_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(pkeys + c0, prows + c0, cn, g.table.as<Slot>(),
+                                                                 g.jmask, sc, nwt, per_warp, part,
+                                                                 g.jflags.as<unsigned int>());
     CKL();
     const bool last = c0 + kSub >= np;
     const unsigned long long* bin = c0 == 0 ? base_in : tmp + ((c0 / kSub) & 1);
     unsigned long long* bout = last ? total_out : tmp + (((c0 / kSub) + 1) & 1);
     scan_partials_kernel<<<1, kScanThreads, 0, s>>>(part, (uint32_t)blocks, bin, bout);
     CKL();
-    join_emit_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(sc, prows + c0, g.csr_row.as<uint32_t>(), nwt,
-                                                                per_block, part, out_p, out_b, cap);
+    join_emit_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(sc, g.rows_arr.as<uint32_t>(), nwt, per_warp, part,
+                                                                out_p, out_b, cap);
     CKL();
     g_launches += 3;
   }
@@ -766,8 +770,8 @@ int golp_shutdown(void) {
   cudaDeviceSynchronize();
   g.pool.stop();
   DevBuf* bufs[] = {&g.ctl, &g.cand_hi, &g.cand_lo, &g.w_hi, &g.w_lo, &g.out_rows, &g.out_hi, &g.samples,
-                    &g.table, &g.bslot, &g.brank, &g.csr_pos, &g.csr_row, &g.big_list, &g.jcount,
-                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_entry, &g.jflags, &g.pairs_p, &g.pairs_b, &g.in_keys, &g.in_rows,
+                    &g.table, &g.rows_arr, &g.ovf, &g.big_list, &g.jcount,
+                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.jflags, &g.pairs_p, &g.pairs_b, &g.in_keys, &g.in_rows,
                     &g.in_bkeys, &g.in_brows, &g.in_payload};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < kSlots; ++i) {
@@ -827,6 +831,11 @@ int golp_last_kernel_times(golp_kernel_times* out) {
     g.kt.join_build_ms = prof_ms(4, 5);
     g.build_timed = false;
   }
+  if (g.probe_timed) {
+    CK(cudaEventSynchronize(g.ev[7]));
+    g.kt.join_probe_ms = prof_ms(6, 7);
+    g.probe_timed = false;
+  }
   *out = g.kt;
   return GOLP_OK;
 }
@@ -860,6 +869,23 @@ int golp_join_build_device(const double* d_build_keys, const uint32_t* d_build_r
   RET(join_build_impl(d_build_keys, d_build_rows, nb, s));
   g.build_timed = g.prof;  // resolved lazily by golp_last_kernel_times (no sync here)
   g.kt.join_capacity = g.jcap;
+  return GOLP_OK;
+}
+
+int golp_join_probe_device_async(const double* d_probe_keys, const uint32_t* d_probe_rows, uint64_t np,
+                                 uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
+                                 uint64_t* d_out_matches, void* stream) {
+  RET(ensure_init());
+  if (!d_out_matches) return invalid("null d_out_matches");
+  cudaStream_t s = as_stream(stream);
+  CK(g.totals.ensure(16));
+  unsigned long long* totals = g.totals.as<unsigned long long>();
+  CK(cudaMemsetAsync(totals, 0, 8, s));
+  prof_record(6, s);
+  RET(launch_probe(d_probe_keys, d_probe_rows, np, d_out_probe_rows, d_out_build_rows, cap, totals,
+                   reinterpret_cast<unsigned long long*>(d_out_matches), s));
+  prof_record(7, s);
+  g.probe_timed = g.prof;  // resolved lazily by golp_last_kernel_times
   return GOLP_OK;
 }
 

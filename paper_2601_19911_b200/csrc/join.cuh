@@ -11,11 +11,12 @@
 //            DISTINCT build key. Linear probing whose start is rounded down to an
 //            even slot: the probe walks 32-byte, sector-aligned slot pairs, one
 //            256-bit load per pair (LDG.E.256). cap = pow2 >= 2*nb (load <= 0.5).
-//   csr_row: nb x u32, the build rows of every key group in build-position order;
-//            groups of one keep their row inline in slot.off (no CSR access).
-// Build: insert (atomicCAS) -> group offsets (warp-aggregated cursor) -> scatter
-// build positions -> per-group sort of positions (thread / block / block-global)
-// -> rows. Probe: match (one lookup per probe, compacted per warp tile) -> scan
+//   rows   : cap*kInline + nb u32: groups of 2..kInline keep their rows at
+//            h*kInline, bigger groups a CSR range after that, all in build-position
+//            order; groups of one keep their row inline in slot.off.
+// Build: insert (atomicCAS claim, atomicAdd rank, first kInline positions into a
+// slot-indexed side array) -> one pass over the slots finalizes every group ->
+// overflow members and big-group sorts (rare). Probe: match (one lookup per probe, compacted per warp tile) -> scan
 // -> emit (see below).
 #pragma once
 #include <cooperative_groups.h>
@@ -35,8 +36,17 @@ __host__ __device__ __forceinline__ uint64_t home_slot(uint64_t bits, uint64_t m
   return mix64(bits) & mask & ~1ull;
 }
 
-constexpr int kSmallGroup = 32;        // groups up to this size sorted by their leader thread
-constexpr uint32_t kGroupTile = 16384;  // groups up to this size sorted in shared memory (64 KB)
+// Key groups: the first kInline build positions of every group are recorded in
+// a slot-indexed side array while inserting (rows[h*kInline + rank]); one pass
+// over the slots then finalizes each group:
+//   cnt == 1        slot.off = the build row (probe reads no side array)
+//   2..kInline      positions sorted in place and turned into rows; slot.off = h*kInline
+//   > kInline       a CSR range [off, off+cnt) after the side array; members of
+//                   rank >= kInline come from an overflow list; one block sorts
+// so no per-entry slot/rank arrays and no offset/fill/sort chain are needed for
+// the common (small) groups. Probe: cnt >= 2 reads rows[off + m].
+constexpr uint32_t kInline = 4;
+constexpr uint32_t kGroupTile = 16384;  // big groups up to this size sorted in shared memory (64 KB)
 
 __global__ void join_init_table_kernel(Slot* __restrict__ table, uint64_t cap) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -52,10 +62,17 @@ constexpr int kBuildThreads = 256;
 constexpr int kBuildItems = 4;
 constexpr uint64_t kBuildTile = (uint64_t)kBuildThreads * kBuildItems;
 
+struct GroupArrays {
+  uint32_t* rows;        // kInline per slot, then CSR ranges of big groups
+  uint32_t* ovf_slot;    // overflow members (rank >= kInline)
+  uint32_t* ovf_rank;
+  uint32_t* ovf_pos;
+  unsigned long long* counters;  // [0] overflow count, [1] CSR cursor, [2] big groups, [3] of them > kThreadGroup
+  uint32_t* big_list;  // big groups, then (appended) the ones above kThreadGroup
+};
+
 __global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double* __restrict__ bkeys, uint64_t nb,
-                                                                    Slot* table, uint64_t mask,
-                                                                    uint32_t* __restrict__ bslot,
-                                                                    uint32_t* __restrict__ brank) {
+                                                                    Slot* table, uint64_t mask, GroupArrays ga) {
   for (uint64_t t0 = (uint64_t)blockIdx.x * kBuildTile; t0 < nb; t0 += (uint64_t)gridDim.x * kBuildTile) {
     uint64_t b[kBuildItems];
     uint32_t h[kBuildItems];
@@ -67,7 +84,7 @@ __global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double
       h[j] = (uint32_t)home_slot(b[j], mask);
       if (i < nb) pending |= 1u << j;
     }
-    unsigned valid = pending;
+    const unsigned valid = pending;
     // Claim or find each key's slot: CAS issued for every pending entry at once.
     while (pending) {
       unsigned long long old[kBuildItems];
@@ -90,136 +107,131 @@ __global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double
 #pragma unroll
     for (int j = 0; j < kBuildItems; ++j) {
       const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
-      if (valid & (1u << j)) {
-        bslot[i] = h[j];
-        brank[i] = r[j];
+      const bool ok = (valid >> j) & 1u;
+      if (ok && r[j] < kInline) ga.rows[(uint64_t)h[j] * kInline + r[j]] = (uint32_t)i;
+      const bool ovf = ok && r[j] >= kInline;
+      const unsigned long long k = warp_append(&ga.counters[0], ovf);
+      if (ovf) {
+        ga.ovf_slot[k] = h[j];
+        ga.ovf_rank[k] = r[j];
+        ga.ovf_pos[k] = (uint32_t)i;
       }
     }
   }
 }
 
-// One leader per group (rank 0) reserves the group's CSR range; groups of one
-// keep their row inline in slot.off and reserve nothing.
-__global__ void __launch_bounds__(kBuildThreads) join_offsets_kernel(uint64_t nb, Slot* table,
-                                                                     const uint32_t* __restrict__ bslot,
-                                                                     const uint32_t* __restrict__ brank,
-                                                                     const uint32_t* __restrict__ brows,
-                                                                     unsigned long long* cursor, uint32_t* big_list,
-                                                                     unsigned int* big_count) {
+__device__ __forceinline__ void cswap_u32(uint32_t& a, uint32_t& b) {
+  const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
+  a = lo;
+  b = hi;
+}
+
+// One pass over the slots: singletons inline their row, groups of 2..kInline sort
+// their recorded positions and turn them into rows, big groups reserve a CSR range.
+__global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_t cap, const uint32_t* __restrict__ brows,
+                                                            GroupArrays ga, uint64_t csr_base) {
   const unsigned lane = lane_id();
-  for (uint64_t t0 = (uint64_t)blockIdx.x * kBuildTile; t0 < nb; t0 += (uint64_t)gridDim.x * kBuildTile) {
-    uint32_t h[kBuildItems], cnt[kBuildItems], rk[kBuildItems];
-#pragma unroll
-    for (int j = 0; j < kBuildItems; ++j) {
-      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
-      rk[j] = i < nb ? brank[i] : 1u;
-      h[j] = i < nb ? bslot[i] : 0u;
-    }
-#pragma unroll
-    for (int j = 0; j < kBuildItems; ++j) cnt[j] = rk[j] == 0 ? table[h[j]].cnt : 0u;
-#pragma unroll
-    for (int j = 0; j < kBuildItems; ++j) {
-      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
-      if (cnt[j] == 1) table[h[j]].off = __ldg(brows + i);  // singleton: inline row
-      const uint32_t need = cnt[j] > 1 ? cnt[j] : 0u;
-      unsigned long long incl = need;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if ((int)lane >= o) incl += v;
-      }
-      unsigned long long base = 0;
-      if (lane == 31 && incl) base = atomicAdd(cursor, incl);
-      base = __shfl_sync(0xFFFFFFFFu, base, 31);
-      if (need) {
-        table[h[j]].off = (uint32_t)(base + incl - need);
-        if (need > (uint32_t)kSmallGroup) big_list[atomicAdd(big_count, 1u)] = h[j];
-      }
-    }
-  }
-}
-
-// Members of multi-entry groups scatter their build positions into the group's range.
-__global__ void __launch_bounds__(kBuildThreads) join_fill_kernel(uint64_t nb, const Slot* __restrict__ table,
-                                                                  const uint32_t* __restrict__ bslot,
-                                                                  const uint32_t* __restrict__ brank,
-                                                                  uint32_t* __restrict__ csr_pos) {
-  for (uint64_t t0 = (uint64_t)blockIdx.x * kBuildTile; t0 < nb; t0 += (uint64_t)gridDim.x * kBuildTile) {
-    uint32_t h[kBuildItems], rk[kBuildItems];
-    uint2 oc[kBuildItems];
-#pragma unroll
-    for (int j = 0; j < kBuildItems; ++j) {
-      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
-      h[j] = i < nb ? bslot[i] : 0u;
-      rk[j] = i < nb ? brank[i] : 0u;
-    }
-#pragma unroll
-    for (int j = 0; j < kBuildItems; ++j) {
-      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
-      oc[j] = i < nb ? *reinterpret_cast<const uint2*>(&table[h[j]].off) : make_uint2(0, 1);
-    }
-#pragma unroll
-    for (int j = 0; j < kBuildItems; ++j) {
-      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
-      if (i < nb && oc[j].y > 1) csr_pos[oc[j].x + rk[j]] = (uint32_t)i;
-    }
-  }
-}
-
-// Groups of 2..kSmallGroup: the leader sorts the positions and writes rows.
-__global__ void __launch_bounds__(kBuildThreads) join_small_groups_kernel(uint64_t nb, const Slot* __restrict__ table,
-                                                                          const uint32_t* __restrict__ bslot,
-                                                                          const uint32_t* __restrict__ brank,
-                                                                          const uint32_t* __restrict__ csr_pos,
-                                                                          const uint32_t* __restrict__ brows,
-                                                                          uint32_t* __restrict__ csr_row) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += stride) {
-    if (brank[i] != 0) continue;
-    const uint32_t h = bslot[i];
-    const uint2 oc = *reinterpret_cast<const uint2*>(&table[h].off);
-    const uint32_t cnt = oc.y;
-    if (cnt < 2 || cnt > (uint32_t)kSmallGroup) continue;
-    const uint32_t off = oc.x;
-    if (cnt == 2) {  // the common case: one compare
-      const uint32_t a = csr_pos[off], b = csr_pos[off + 1];
-      const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
-      csr_row[off] = __ldg(brows + lo);
-      csr_row[off + 1] = __ldg(brows + hi);
+  for (uint64_t wb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; wb < cap; wb += stride) {
+    const uint64_t h = wb + lane;
+    uint32_t cnt = 0;
+    if (h < cap) {
+      const ulonglong2 sl = reinterpret_cast<const ulonglong2*>(table)[h];
+      if (sl.x != kEmptyKey) cnt = (uint32_t)(sl.y >> 32);
+    }
+    uint32_t* grp = ga.rows + h * kInline;
+    if (cnt == 1) {
+      table[h].off = __ldg(brows + grp[0]);
+    } else if (cnt >= 2 && cnt <= kInline) {
+      const uint4 v = *reinterpret_cast<const uint4*>(grp);
+      uint32_t p0 = v.x, p1 = v.y, p2 = cnt > 2 ? v.z : 0xFFFFFFFFu, p3 = cnt > 3 ? v.w : 0xFFFFFFFFu;
+      cswap_u32(p0, p1); cswap_u32(p2, p3); cswap_u32(p0, p2); cswap_u32(p1, p3); cswap_u32(p1, p2);
+      uint4 o;
+      o.x = __ldg(brows + p0);
+      o.y = __ldg(brows + p1);
+      o.z = cnt > 2 ? __ldg(brows + p2) : 0u;
+      o.w = cnt > 3 ? __ldg(brows + p3) : 0u;
+      *reinterpret_cast<uint4*>(grp) = o;
+      table[h].off = (uint32_t)(h * kInline);
+    }
+    const uint32_t need = cnt > kInline ? cnt : 0u;  // big group: reserve its CSR range
+    unsigned long long incl = need;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if ((int)lane >= o) incl += v;
+    }
+    unsigned long long base = 0;
+    if (lane == 31 && incl) base = atomicAdd(&ga.counters[1], incl);
+    base = __shfl_sync(0xFFFFFFFFu, base, 31);
+    if (need) {
+      const uint64_t off = csr_base + base + incl - need;
+      table[h].off = (uint32_t)off;
+      const uint4 v = *reinterpret_cast<const uint4*>(grp);  // ranks 0..3
+      ga.rows[off] = v.x;
+      ga.rows[off + 1] = v.y;
+      ga.rows[off + 2] = v.z;
+      ga.rows[off + 3] = v.w;
+      ga.big_list[atomicAdd(&ga.counters[2], 1ull)] = (uint32_t)h;
+    }
+  }
+}
+
+// Overflow members (rank >= kInline) land at their rank inside their group's range.
+__global__ void join_overflow_kernel(const Slot* __restrict__ table, GroupArrays ga) {
+  const unsigned long long n = *(volatile unsigned long long*)&ga.counters[0];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride)
+    ga.rows[table[ga.ovf_slot[k]].off + ga.ovf_rank[k]] = ga.ovf_pos[k];
+}
+
+// Big groups of up to kThreadGroup members: one thread sorts the positions
+// (insertion sort) and writes rows; larger ones are queued for the block kernel.
+constexpr uint32_t kThreadGroup = 32;
+
+__global__ void join_group_sort_kernel(const Slot* __restrict__ table, GroupArrays ga,
+                                       const uint32_t* __restrict__ brows) {
+  const unsigned nbig = (unsigned)*(volatile unsigned long long*)&ga.counters[2];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < nbig; gi += stride) {
+    const uint32_t h = ga.big_list[gi];
+    const uint32_t cnt = table[h].cnt;
+    if (cnt > kThreadGroup) {
+      ga.big_list[nbig + atomicAdd(&ga.counters[3], 1ull)] = h;  // block kernel's queue
       continue;
     }
-    uint32_t p[kSmallGroup];
+    uint32_t* seg = ga.rows + table[h].off;
+    uint32_t p[kThreadGroup];
     for (uint32_t m = 0; m < cnt; ++m) {
-      const uint32_t v = csr_pos[off + m];
+      const uint32_t v = seg[m];
       uint32_t q = m;
       while (q > 0 && p[q - 1] > v) { p[q] = p[q - 1]; --q; }
       p[q] = v;
     }
-    for (uint32_t m = 0; m < cnt; ++m) csr_row[off + m] = __ldg(brows + p[m]);
+    for (uint32_t m = 0; m < cnt; ++m) seg[m] = __ldg(brows + p[m]);
   }
 }
 
-// Groups > kSmallGroup: one block per group; shared-memory sort up to kGroupTile,
-// in-place global network beyond (pathological duplicate counts only).
-__global__ void __launch_bounds__(1024) join_big_groups_kernel(const Slot* __restrict__ table,
-                                                               const uint32_t* __restrict__ big_list,
-                                                               const unsigned int* __restrict__ big_count,
-                                                               uint32_t* csr_pos, const uint32_t* __restrict__ brows,
-                                                               uint32_t* __restrict__ csr_row) {
+// Groups above kThreadGroup (queued by join_group_sort_kernel): one block per
+// group sorts its positions (shared memory up to kGroupTile, in place in global
+// memory beyond) and turns them into rows.
+__global__ void __launch_bounds__(1024) join_big_groups_kernel(const Slot* __restrict__ table, GroupArrays ga,
+                                                               const uint32_t* __restrict__ brows) {
   extern __shared__ __align__(16) uint32_t s_pos[];
-  const unsigned nbig = *big_count;
-  for (unsigned g = blockIdx.x; g < nbig; g += gridDim.x) {
-    const uint32_t h = big_list[g];
+  const unsigned nbig = (unsigned)*(volatile unsigned long long*)&ga.counters[2];
+  const unsigned nhuge = (unsigned)*(volatile unsigned long long*)&ga.counters[3];
+  for (unsigned gi = blockIdx.x; gi < nhuge; gi += gridDim.x) {
+    const uint32_t h = ga.big_list[nbig + gi];
     const uint32_t cnt = table[h].cnt;
-    const uint32_t off = table[h].off;
+    uint32_t* seg = ga.rows + table[h].off;
     if (cnt <= kGroupTile) {
-      for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) s_pos[m] = csr_pos[off + m];
+      for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) s_pos[m] = seg[m];
       __syncthreads();
       block_sort_asc_u32<false>(s_pos, cnt);
-      for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) csr_row[off + m] = __ldg(brows + s_pos[m]);
+      for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) seg[m] = __ldg(brows + s_pos[m]);
     } else {
-      block_sort_asc_u32<true>(csr_pos + off, cnt);
-      for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) csr_row[off + m] = __ldg(brows + __ldcg(csr_pos + off + m));
+      block_sort_asc_u32<true>(seg, cnt);
+      for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) seg[m] = __ldg(brows + __ldcg(seg + m));
     }
     __syncthreads();
   }
@@ -229,16 +241,14 @@ __global__ void __launch_bounds__(1024) join_big_groups_kernel(const Slot* __res
 // Bound by random table lookups: ~1 L1TEX wavefront per lookup, ~0.8/clk/SM
 // from L2 (tools/microbench.cu, tools/probe_ladder.cu). Every probe key is looked
 // up exactly once:
-//   match : each block walks a contiguous range of warp tiles (32*kWarpItems
-//           consecutive probes); a warp resolves its probes (linear probing over
-//           32-byte slot pairs) and
-//           compacts the hits, in probe order, into the tile's scratch segment as
-//           8-byte entries {slot.off, slot.cnt << 8 | position in tile};
-//           per-tile entry / pair counts and the block's pair total are written.
+//   match : each warp walks a contiguous run of warp tiles (32*kWarpItems
+//           consecutive probes each), resolves its probes (linear probing over
+//           32-byte slot pairs) and appends the hits, in probe order, to its own
+//           contiguous scratch segment {probe row, slot.off, slot.cnt}; per-warp
+//           entry / pair counts and per-block pair totals are written.
 //   scan  : one block scans the per-block totals (+ pairs of earlier launches).
-//   emit  : same block -> tile-range mapping; a block scan of the tiles' pair
-//           counts gives each tile's output offset; warps expand entries to
-//           (probe row, build row) pairs.
+//   emit  : same mapping; each warp streams its segment to the output at its
+//           offset (block offset + pairs of the block's earlier warps).
 // Output order = probe position, then CSR (build insertion) order.
 #ifndef GOLP_WARP_ITEMS
 #define GOLP_WARP_ITEMS 2
@@ -247,10 +257,9 @@ __global__ void __launch_bounds__(1024) join_big_groups_kernel(const Slot* __res
 #define GOLP_PROBE_MINB 6
 #endif
 constexpr int kWarpItems = GOLP_WARP_ITEMS;
+static_assert(kWarpItems % 2 == 0, "keys are loaded as 16-byte pairs");
 constexpr uint32_t kWarpTile = 32 * kWarpItems;  // probes per warp tile
-static_assert(kWarpTile <= 256, "entry position is 8 bits");
 constexpr int kProbeThreads = 256;
-constexpr uint32_t kMaxTilesPerBlock = 4096;
 constexpr uint32_t kMaxGroup = (1u << 24) - 1;  // largest key group an entry can describe
 
 // L2 eviction policies: the table should survive the probe stream in L2, the
@@ -351,25 +360,35 @@ __device__ __forceinline__ int check_pair(const ulonglong4& sl, uint64_t bits, u
   return -1;
 }
 
+// Scratch entries are SoA {probe row, slot.off, slot.cnt}. Each warp owns a
+// contiguous run of warp tiles and appends its hits contiguously (in probe
+// order) starting at its first tile's slot, so emit is a streaming copy.
 struct MatchScratch {
-  uint2* entry;      // kWarpTile per warp tile: {slot.off, cnt << 8 | pos}
-  uint32_t* nmatch;  // per warp tile
-  uint32_t* npairs;  // per warp tile
+  uint32_t* prow;
+  uint32_t* off;
+  uint32_t* cnt;
+  uint32_t* wentries;  // per global warp: entries written
+  uint32_t* wpairs;    // per global warp: pairs produced (sum of cnt)
 };
 
+constexpr unsigned kProbeWarps = kProbeThreads / 32;
+
 __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_kernel(
-    const double* __restrict__ pkeys, uint64_t np, const Slot* __restrict__ table, uint64_t mask, MatchScratch sc,
-    uint64_t nwt, uint64_t per_block, unsigned long long* __restrict__ bpart, unsigned int* __restrict__ flags) {
-  __shared__ unsigned long long s_w[kProbeThreads / 32];
+    const double* __restrict__ pkeys, const uint32_t* __restrict__ prows, uint64_t np, const Slot* __restrict__ table,
+    uint64_t mask, MatchScratch sc, uint64_t nwt, uint64_t per_warp, unsigned long long* __restrict__ bpart,
+    unsigned int* __restrict__ flags) {
+  __shared__ unsigned long long s_w[kProbeWarps];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  constexpr unsigned kWarps = kProbeThreads / 32;
   const uint64_t pol_stream = policy_evict_first(), pol_table = policy_evict_last();
-  const uint64_t lo = blockIdx.x * per_block, hi = lo + per_block < nwt ? lo + per_block : nwt;
+  const uint64_t gw = (uint64_t)blockIdx.x * kProbeWarps + warp;
+  const uint64_t lo = gw * per_warp, hi = lo + per_warp < nwt ? lo + per_warp : nwt;
   const uint32_t pm = (uint32_t)mask;
-  unsigned long long mine = 0;
-  for (uint64_t wt = lo + warp; wt < hi; wt += kWarps) {
+  uint64_t cursor = lo * kWarpTile;  // next free scratch entry of this warp
+  uint64_t pairs_total = 0;
+  for (uint64_t wt = lo; wt < hi; ++wt) {
     const uint64_t first = wt * kWarpTile + lane * kWarpItems;
     double k[kWarpItems];
+    uint32_t r[kWarpItems];
     if (first + kWarpItems <= np && (((uintptr_t)(pkeys + first) & 15) == 0)) {
 #pragma unroll
       for (int j = 0; j < kWarpItems; j += 2) {
@@ -417,93 +436,99 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_ker
       const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
       if ((int)lane >= o) incl += v;
     }
-    uint32_t pairs = npr;
+    uint32_t tpairs = npr;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xFFFFFFFFu, pairs, o);
-    mine += pairs;
-    if (lane == 31) {
-      sc.nmatch[wt] = incl;
-      sc.npairs[wt] = pairs;
-    }
-    uint64_t o = wt * kWarpTile + (incl - nm);
+    for (int o = 16; o > 0; o >>= 1) tpairs += __shfl_xor_sync(0xFFFFFFFFu, tpairs, o);
+    pairs_total += tpairs;
+    const uint32_t tmatch = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (nm) {
 #pragma unroll
-    for (int j = 0; j < kWarpItems; ++j) {
-      if (cnt[j]) {
-        if (cnt[j] > kMaxGroup) atomicOr(flags, 1u);  // host re-runs without the packed entry
-        sc.entry[o++] = make_uint2(off[j], (cnt[j] << 8) | (lane * kWarpItems + j));
+      for (int j = 0; j < kWarpItems; ++j) r[j] = cnt[j] ? __ldg(prows + first + j) : 0u;
+      uint64_t o = cursor + (incl - nm);
+#pragma unroll
+      for (int j = 0; j < kWarpItems; ++j) {
+        if (cnt[j]) {
+          sc.prow[o] = r[j];
+          sc.off[o] = off[j];
+          sc.cnt[o] = cnt[j];
+          ++o;
+        }
       }
     }
+    cursor += tmatch;
   }
-  if (lane == 0) s_w[warp] = mine;
+  if (lane == 0) {
+    sc.wentries[gw] = (uint32_t)(cursor - lo * kWarpTile);
+    sc.wpairs[gw] = (uint32_t)pairs_total;
+    s_w[warp] = pairs_total;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long t = 0;
-    for (unsigned w = 0; w < kWarps; ++w) t += s_w[w];
+    for (unsigned w = 0; w < kProbeWarps; ++w) t += s_w[w];
     bpart[blockIdx.x] = t;
   }
+  (void)flags;
 }
 
-__global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch sc, const uint32_t* __restrict__ prows,
-                                                                  const uint32_t* __restrict__ csr_row, uint64_t nwt,
-                                                                  uint64_t per_block,
+// Same block/warp -> tile mapping as join_match_kernel. bpart holds the exclusive
+// offsets of the blocks (scan_partials_kernel); a warp's offset adds the pairs of
+// the earlier warps of its block. Singletons (slot.off is the build row) are a
+// straight coalesced copy; key groups expand their CSR run.
+__global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch sc, const uint32_t* __restrict__ csr_row,
+                                                                  uint64_t nwt, uint64_t per_warp,
                                                                   const unsigned long long* __restrict__ bpart,
                                                                   uint32_t* __restrict__ out_p,
                                                                   uint32_t* __restrict__ out_b, uint64_t cap) {
-  __shared__ unsigned long long s_off[kMaxTilesPerBlock];
-  __shared__ unsigned long long s_w[33];
+  __shared__ unsigned long long s_wp[kProbeWarps];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  constexpr unsigned kWarps = kProbeThreads / 32;
-  const uint64_t lo = blockIdx.x * per_block, hi = lo + per_block < nwt ? lo + per_block : nwt;
-  if (lo >= hi) return;
-  const uint32_t n = (uint32_t)(hi - lo);
-  unsigned long long carry = bpart[blockIdx.x];
-  for (uint32_t b0 = 0; b0 < n; b0 += kProbeThreads) {
-    const uint32_t i = b0 + threadIdx.x;
-    const unsigned long long v = i < n ? sc.npairs[lo + i] : 0ull;
-    unsigned long long t;
-    const unsigned long long e = block_excl_scan(v, s_w, &t);
-    if (i < n) s_off[i] = carry + e;
-    carry += t;
-  }
+  const uint64_t gw = (uint64_t)blockIdx.x * kProbeWarps + warp;
+  const uint64_t lo = gw * per_warp;
+  if (lane == 0) s_wp[warp] = lo < nwt ? sc.wpairs[gw] : 0ull;
   __syncthreads();
+  unsigned long long run = bpart[blockIdx.x];
+  for (unsigned w = 0; w < warp; ++w) run += s_wp[w];
+  if (lo >= nwt) return;
   const uint64_t pol_stream = policy_evict_first();
-  for (uint64_t t = lo + warp; t < hi; t += kWarps) {
-    const uint32_t nm = sc.nmatch[t];
-    if (nm == 0) continue;
-    unsigned long long run = s_off[t - lo];
-    const uint64_t e0 = t * kWarpTile;
-    for (uint32_t i0 = 0; i0 < nm; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      uint32_t c = 0, pr = 0, of = 0;
-      if (i < nm) {
-        const uint2 en = __ldcs(sc.entry + e0 + i);
-        of = en.x;
-        c = en.y >> 8;
-        pr = __ldg(prows + e0 + (en.y & 255u));
+  const uint64_t e0 = lo * kWarpTile;
+  const uint32_t ne = sc.wentries[gw];
+  constexpr int kBatch = 4;  // 4 x 32 entries in flight per warp iteration
+  for (uint32_t i0 = 0; i0 < ne; i0 += 32 * kBatch) {
+    uint32_t c[kBatch], pr[kBatch], of[kBatch];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const uint32_t i = i0 + q * 32 + lane;
+      c[q] = 0;
+      pr[q] = 0;
+      of[q] = 0;
+      if (i < ne) {
+        c[q] = __ldcs(sc.cnt + e0 + i);
+        pr[q] = __ldcs(sc.prow + e0 + i);
+        of[q] = __ldcs(sc.off + e0 + i);
       }
-      uint32_t incl = c;
+    }
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      uint32_t incl = c[q];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if ((int)lane >= o) incl += v;
       }
-      const uint32_t gtot = __shfl_sync(0xFFFFFFFFu, incl, 31);
-      // singletons (slot.off is the build row) land at consecutive positions;
-      // the rare multi-match entries expand their CSR run serially
-      unsigned long long g = run + (incl - c);
-      if (c == 1) {
+      unsigned long long g = run + (incl - c[q]);
+      if (c[q] == 1) {
         if (g < cap) {
-          st_hint(out_p + g, pr, pol_stream);
-          st_hint(out_b + g, of, pol_stream);
+          st_hint(out_p + g, pr[q], pol_stream);
+          st_hint(out_b + g, of[q], pol_stream);
         }
       } else {
-        for (uint32_t m = 0; m < c; ++m, ++g)
+        for (uint32_t m = 0; m < c[q]; ++m, ++g)
           if (g < cap) {
-            st_hint(out_p + g, pr, pol_stream);
-            st_hint(out_b + g, __ldg(csr_row + of + m), pol_stream);
+            st_hint(out_p + g, pr[q], pol_stream);
+            st_hint(out_b + g, __ldg(csr_row + of[q] + m), pol_stream);
           }
       }
-      run += gtot;
+      run += __shfl_sync(0xFFFFFFFFu, incl, 31);
     }
   }
 }

@@ -80,6 +80,18 @@ def join_probe(keys: torch.Tensor, rows: torch.Tensor, out_probe: torch.Tensor, 
     return int(m.value)
 
 
+def join_probe_async(keys: torch.Tensor, rows: torch.Tensor, out_probe: torch.Tensor, out_build: torch.Tensor,
+                     matches: torch.Tensor, stream=None) -> None:
+    """Enqueue a probe of the last built table without synchronizing; the match
+    count lands in `matches` (int64 CUDA tensor of one element). Pairs beyond the
+    buffers' capacity are dropped: compare matches with the capacity afterwards."""
+    _check_cols(keys, rows)
+    cap = min(out_probe.numel(), out_build.numel())
+    _native.check(_native.load().golp_join_probe_device_async(keys.data_ptr(), rows.data_ptr(), keys.numel(),
+                                                              out_probe.data_ptr(), out_build.data_ptr(), cap,
+                                                              matches.data_ptr(), _stream(stream)))
+
+
 def join(bkeys, brows, pkeys, prows, capacity: int | None = None, stream=None):
     """Build + probe -> (probe_rows[M], build_rows[M]) int32 tensors."""
     join_build(bkeys, brows, stream)

@@ -14,11 +14,10 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 VDIR = ROOT / "paper_2601_19911_b200" / "variants"
 VARIANTS = {
-    "w4_b4": ["GOLP_WARP_ITEMS=4", "GOLP_PROBE_MINB=4"],
-    "w4_b3": ["GOLP_WARP_ITEMS=4", "GOLP_PROBE_MINB=3"],
-    "w4_b5": ["GOLP_WARP_ITEMS=4", "GOLP_PROBE_MINB=5"],
-    "w2_b8": ["GOLP_WARP_ITEMS=2", "GOLP_PROBE_MINB=8"],
     "w2_b6": ["GOLP_WARP_ITEMS=2", "GOLP_PROBE_MINB=6"],
+    "w2_b8": ["GOLP_WARP_ITEMS=2", "GOLP_PROBE_MINB=8"],
+    "w4_b4": ["GOLP_WARP_ITEMS=4", "GOLP_PROBE_MINB=4"],
+    "w4_b6": ["GOLP_WARP_ITEMS=4", "GOLP_PROBE_MINB=6"],
 }
 
 
