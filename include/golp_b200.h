@@ -158,6 +158,11 @@ int golp_host_hash_probe(const uint64_t* slot_bits, const uint32_t* slot_rows, u
                          uint64_t* out_matches);
 /* Phase 2: copy the M pairs of the last golp_host_hash_probe, reference order. */
 int golp_host_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m);
+/* Late materialization (store.materialize, store.py:184-201, and its join
+ * counterpart): dst[i] = src row ids[i] (row_bytes each), multi-threaded;
+ * an id >= nrows -> GOLP_ERR_INVALID. */
+int golp_host_gather(const void* src, uint64_t row_bytes, uint64_t nrows, const uint32_t* ids, uint64_t n, void* dst,
+                     int threads);
 
 #ifdef __cplusplus
 }

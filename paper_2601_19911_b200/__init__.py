@@ -70,12 +70,14 @@ from .store import (
     KEY_ENTRY_BYTES,
     ColumnTable,
     KeyVector,
+    MaterializedJoin,
     MaterializedResult,
     extract_keys,
     full_row_bytes,
     generate_table,
     key_only_bytes,
     materialize,
+    materialize_join,
     random_key_vector,
     random_keys,
 )

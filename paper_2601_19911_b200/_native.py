@@ -84,6 +84,7 @@ SIGNATURES = {
     "golp_host_hash_build": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),
     "golp_host_hash_probe": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, _int, C.POINTER(_u64)]),
     "golp_host_probe_copy_out": (_int, [_vp, _vp, _u64]),
+    "golp_host_gather": (_int, [_vp, _u64, _u64, _vp, _u64, _vp, _int]),
 }
 
 _lib = None

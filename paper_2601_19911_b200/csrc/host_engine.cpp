@@ -135,6 +135,39 @@ int golp_host_hash_probe(const uint64_t* slot_bits, const uint32_t* slot_rows, u
   return GOLP_OK;
 }
 
+int golp_host_gather(const void* src, uint64_t row_bytes, uint64_t nrows, const uint32_t* ids, uint64_t n, void* dst,
+                     int threads) {
+  if (n == 0) return GOLP_OK;
+  if (!src || !ids || !dst || row_bytes == 0) return invalid("null buffer");
+  WorkerPool& pool = host_pool();
+  uint64_t parts = threads > 0 ? (uint64_t)threads : (uint64_t)pool.size() + 1;
+  parts = std::max<uint64_t>(1, std::min<uint64_t>(parts, n / 16384 + 1));
+  const uint64_t step = (n + parts - 1) / parts;
+  std::atomic<bool> bad{false};
+  const char* s = static_cast<const char*>(src);
+  char* d = static_cast<char*>(dst);
+  pool.run(parts, [&](size_t t) {
+    const uint64_t lo = t * step, hi = std::min(n, lo + step);
+    if (row_bytes == 8) {
+      const uint64_t* s8 = static_cast<const uint64_t*>(src);
+      uint64_t* d8 = static_cast<uint64_t*>(dst);
+      for (uint64_t i = lo; i < hi; ++i) {
+        const uint32_t r = ids[i];
+        if (r >= nrows) { bad = true; return; }
+        d8[i] = s8[r];
+      }
+      return;
+    }
+    for (uint64_t i = lo; i < hi; ++i) {
+      const uint32_t r = ids[i];
+      if (r >= nrows) { bad = true; return; }
+      std::memcpy(d + i * row_bytes, s + (uint64_t)r * row_bytes, row_bytes);
+    }
+  });
+  if (bad) return invalid("row id out of range");
+  return GOLP_OK;
+}
+
 int golp_host_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m) {
   if (m != g_probe_m) return invalid("copy_out size does not match the last host probe");
   uint64_t o = 0;

@@ -157,3 +157,23 @@ def test_execute_gated_topk_and_probe_on_host_path():
     assert np.all(np.diff(res.keys) <= 0)
     res2, d2, _ = execute_gated((generate_table(300, 8, seed=1), t), OP_PROBE, 1, GateConfig())
     assert d2.path == HOST and res2.probe_count == 5000
+
+
+def test_materialize_join_gathers_both_sides_in_pair_order():
+    from paper_2601_19911_b200 import host_hash_build, host_hash_probe, extract_keys, materialize_join
+
+    b = generate_table(2000, 12, seed=4)
+    p = generate_table(5000, 7, seed=5)
+    # small key domain so the tables actually join
+    b = type(b)(np.floor(b.key_column / 2**45), b.payload_column)
+    p = type(p)(np.floor(p.key_column / 2**45), p.payload_column)
+    res = host_hash_probe(host_hash_build(extract_keys(b)), extract_keys(p))
+    assert res.match_count > 100
+    mj = materialize_join(b, p, res)
+    assert len(mj) == res.match_count
+    assert np.array_equal(mj.probe.keys, mj.build.keys)  # joined on equal keys
+    assert np.array_equal(mj.build.payloads, b.payload_column[res.build_rows])
+    assert np.array_equal(mj.probe.payloads, p.payload_column[res.probe_rows])
+    bad = type(res)(np.array([0], np.uint32), np.array([10**6], np.uint32), 1)
+    with pytest.raises(IndexError):
+        materialize_join(b, p, bad)

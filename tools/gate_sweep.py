@@ -55,10 +55,28 @@ def main(out_path):
         runs = run_strategy_comparison(spec, cfg, device=dev)
         strat[label] = {r.strategy: {**{k: getattr(compute_stats(r.all_samples()), k) for k in ("median", "p95", "p99")},
                                      "offload_rate": r.offload_rate} for r in runs}
+    # the paper's key-only vs full-row experiment on the B200:
+    # Top-K K=100, payload 188 B; E2E full-row = h2d+kernel+d2h, key-only = whole
+    # ledger incl. late materialization (run_payload_comparison semantics)
+    from paper_2601_19911_b200.harness import run_payload_comparison
+
+    pay = run_payload_comparison(WorkloadSpec(n_grid=(1_000_000, 3_000_000, 10_000_000), repeats=1, k=100,
+                                              payload_bytes=188), device=dev)
+    pay = run_payload_comparison(WorkloadSpec(n_grid=(1_000_000, 3_000_000, 10_000_000), repeats=1, k=100,
+                                              payload_bytes=188), device=dev)  # second pass: warm
+    payload = {"transfer": [r._asdict() for r in pay.transfer_rows], "e2e": [r._asdict() for r in pay.e2e_rows],
+               "transfer_time_ratio_full_over_key": {
+                   str(n): next(r.transfer_s for r in pay.payload_rows if r.n == n and r.mode == FULL_ROW) /
+                   next(r.transfer_s for r in pay.payload_rows if r.n == n and r.mode == KEY_ONLY)
+                   for n in (1_000_000, 3_000_000, 10_000_000)}}
     out = {"profile_b200": prof.to_json_dict(), "cpu_model_host_engine": cpu.to_json_dict(),
-           "decisions": grid, "strategy_80_20_stream": strat, "wall_s": time.time() - t0}
+           "decisions": grid, "strategy_80_20_stream": strat, "key_only_vs_full_row": payload,
+           "wall_s": time.time() - t0}
     Path(out_path).write_text(json.dumps(out, indent=1))
-    print(json.dumps({"profile": out["profile_b200"], "strategies": strat}, indent=1))
+    print(json.dumps({"profile": out["profile_b200"], "strategies": strat,
+                      "payload_ratio": payload["transfer_time_ratio_full_over_key"],
+                      "e2e_speedup": [(r["n"], r["mode"], r["speedup_vs_full_row"]) for r in payload["e2e"]]},
+                     indent=1))
     dev.close()
 
 
