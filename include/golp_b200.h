@@ -64,6 +64,7 @@ typedef struct golp_kernel_times {
   uint64_t topk_fallback;   /* 1 if the exact direct path had to run       */
   uint64_t join_groups;     /* distinct build keys                         */
   uint64_t join_capacity;   /* hash-table slots                            */
+  uint64_t join_slices;     /* table slices of a radix-partitioned join (1 = not partitioned) */
 } golp_kernel_times;
 
 /* ---- lifecycle ---------------------------------------------------------------- */

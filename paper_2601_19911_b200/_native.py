@@ -54,6 +54,7 @@ class KernelTimes(C.Structure):
         ("topk_fallback", C.c_uint64),
         ("join_groups", C.c_uint64),
         ("join_capacity", C.c_uint64),
+        ("join_slices", C.c_uint64),
     ]
 
 

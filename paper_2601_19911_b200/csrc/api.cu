@@ -108,10 +108,13 @@ struct Ctx {
 
   DevBuf ctl, cand_hi, cand_lo, w_hi, w_lo, out_rows, out_hi, samples;
   DevBuf table, rows_arr, ovf, big_list, jcount, wcount, partial, totals, totals2;
-  DevBuf sc_prow, sc_off, sc_cnt, jflags;
+  DevBuf sc_prow, sc_off, sc_cnt;
+  DevBuf part_keys, part_pos, part_cnt, part_cur, run_base, run_len, res_part, work_ctr;
   DevBuf pairs_p, pairs_b;
   DevBuf in_keys, in_rows, in_bkeys, in_brows, in_payload;
   uint64_t jcap = 0, jmask = 0, jnb = 0;
+  uint32_t jparts = 1;  // table slices of the radix-partitioned join (1 = not partitioned)
+  int jslice_bits = 0;
   uint64_t last_m = 0;
   bool last_probe_valid = false;
 
@@ -305,10 +308,8 @@ int ensure_chunk_events(size_t n) {
 // Publishes a device counter to mapped pinned host memory with a one-thread
 // kernel: a memcpy here would sit in the D2H copy queue ahead of the pair
 // downloads and block them (head-of-line) until its stream dependency clears.
-__global__ void publish_u64_kernel(volatile unsigned long long* host_dst, const unsigned long long* src,
-                                   volatile unsigned int* host_flag, const unsigned int* flag) {
+__global__ void publish_u64_kernel(volatile unsigned long long* host_dst, const unsigned long long* src) {
   *host_dst = *src;
-  if (host_flag) *host_flag = *flag;
   __threadfence_system();
 }
 
@@ -593,6 +594,101 @@ int grid_for(uint64_t n, int threads, int per_sm) {
   return (int)b;
 }
 
+// Radix partitioning of the join (see join.cuh): slices of GOLP_JOIN_SLICE_BYTES
+// (default 16 MiB of slots) once the table exceeds two slices, at most
+// kMaxProbeParts slices.
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  char* end = nullptr;
+  const unsigned long long x = strtoull(v, &end, 0);
+  return (end && *end == 0) ? (uint64_t)x : dflt;
+}
+
+void plan_partitions(uint64_t cap) {
+  const uint64_t slice_bytes = std::max<uint64_t>(64, env_u64("GOLP_JOIN_SLICE_BYTES", 16ull << 20));
+  uint64_t parts = 1;
+  if (cap * sizeof(Slot) > 2 * slice_bytes) {
+    while (parts < kMaxProbeParts && cap * sizeof(Slot) / parts > slice_bytes) parts <<= 1;
+  }
+  while (parts > 1 && cap / parts < 2) parts >>= 1;
+  int cap_bits = 0;
+  while ((1ull << cap_bits) < cap) ++cap_bits;
+  int part_bits = 0;
+  while ((1ull << part_bits) < parts) ++part_bits;
+  g.jparts = (uint32_t)parts;
+  g.jslice_bits = cap_bits - part_bits;
+}
+
+// Blocks of `kernel` that fit on the GPU at once: grid-stride kernels that
+// walk partitioned data must not have blocks queued behind the resident ones
+// (a queued block would start its walk far behind the others).
+template <typename K>
+int resident_grid(K kernel, int threads, size_t smem) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  return per_sm * g.sms;
+}
+
+// Groups the entries of [keys, keys+n) by table slice into g.part_keys, with
+// positions (build) or in-tile indices + (tile, slice) runs (probe). 3 launches.
+int partition_entries(const double* keys, uint64_t n, bool probe_side, cudaStream_t s) {
+  const uint32_t P = g.jparts;
+  const uint64_t ntiles = (n + kPartTile - 1) / kPartTile;
+  CK(g.part_keys.ensure(std::max<uint64_t>(n, 1) * 8));
+  CK(g.part_pos.ensure(std::max<uint64_t>(n, 1) * (probe_side ? 2 : 4)));
+  CK(g.part_cnt.ensure(P * 8));
+  CK(g.part_cur.ensure(P * 8));
+  PartOut o{g.part_keys.as<double>(), nullptr, nullptr, nullptr, nullptr};
+  if (probe_side) {
+    CK(g.run_base.ensure(std::max<uint64_t>(ntiles * P, 1) * 4));
+    CK(g.run_len.ensure(std::max<uint64_t>(ntiles * P, 1) * 2));
+    o.idx = g.part_pos.as<uint16_t>();
+    o.run_base = g.run_base.as<uint32_t>();
+    o.run_len = g.run_len.as<uint16_t>();
+  } else {
+    o.pos = g.part_pos.as<uint32_t>();
+  }
+  unsigned long long* cnt = g.part_cnt.as<unsigned long long>();
+  unsigned long long* cur = g.part_cur.as<unsigned long long>();
+  CK(cudaMemsetAsync(cnt, 0, P * 8, s));
+  part_count_kernel<<<g.sms * 2, kPartThreads, 0, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cnt);
+  CKL();
+  part_scan_kernel<<<1, 1024, 0, s>>>(cnt, cur, P);
+  CKL();
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(part_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartSmem));
+    attr = true;
+  }
+  static const int gsmax = resident_grid(part_scatter_kernel, kPartThreads, kPartSmem);
+  const int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)gsmax));
+  part_scatter_kernel<<<gs, kPartThreads, kPartSmem, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cur, o);
+  CKL();
+  g_launches += 3;
+  return GOLP_OK;
+}
+
+// Slice-ordered lookups of [pkeys, pkeys+n): partition by table slice, then
+// g.res_part[i] = packed slot of g.part_keys[i] (4 launches).
+int probe_partitioned(const double* pkeys, uint64_t n, cudaStream_t s) {
+  RET(partition_entries(pkeys, n, true, s));
+  CK(g.res_part.ensure(n * 8));
+  static const int grid = resident_grid(join_probe_part_kernel, kProbeThreads, 0);
+  static const int policy = (int)env_u64("GOLP_JOIN_PART_POLICY", 0);
+  const uint64_t items = (uint64_t)kProbeThreads * kPartProbeItems;
+  const int gp = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + items - 1) / items, (uint64_t)grid));
+  CK(g.work_ctr.ensure(8));
+  CK(cudaMemsetAsync(g.work_ctr.p, 0, 8, s));
+  join_probe_part_kernel<<<gp, kProbeThreads, 0, s>>>(g.part_keys.as<double>(), n, g.table.as<Slot>(), g.jmask,
+                                                      g.res_part.as<uint64_t>(), policy,
+                                                      TileSched{g.work_ctr.as<unsigned long long>()});
+  CKL();
+  ++g_launches;
+  return GOLP_OK;
+}
+
 int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cudaStream_t s) {
   uint64_t cap = 1024;
   while (cap < 2 * nb && cap < (1ull << 32)) cap <<= 1;
@@ -606,10 +702,12 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   CK(g.ovf.ensure(nbb * 12));
   CK(g.big_list.ensure((nbb / (kInline + 1) * 2 + 2) * 4));
   CK(g.jcount.ensure(32));
-  CK(g.jflags.ensure(4));
   g.jcap = cap;
   g.jmask = cap - 1;
   g.jnb = nb;
+  plan_partitions(cap);
+  g.kt.join_capacity = cap;
+  g.kt.join_slices = g.jparts;
   Slot* table = g.table.as<Slot>();
   GroupArrays ga;
   ga.rows = g.rows_arr.as<uint32_t>();
@@ -623,13 +721,27 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   CKL();
   ++g_launches;
   CK(cudaMemsetAsync(g.jcount.p, 0, 32, s));
-  CK(cudaMemsetAsync(g.jflags.p, 0, 4, s));
   if (nb == 0) {
     prof_record(5, s);
     return GOLP_OK;
   }
-  const int gb = grid_for((nb + kBuildItems - 1) / kBuildItems, kBuildThreads, 8);
-  join_insert_kernel<<<gb, kBuildThreads, 0, s>>>(bkeys, nb, table, g.jmask, ga);
+  const double* ikeys = bkeys;
+  const uint32_t* ipos = nullptr;
+  if (g.jparts > 1) {
+    RET(partition_entries(bkeys, nb, false, s));
+    ikeys = g.part_keys.as<double>();
+    ipos = g.part_pos.as<uint32_t>();
+  }
+  int gb = grid_for((nb + kBuildItems - 1) / kBuildItems, kBuildThreads, 8);
+  TileSched sched{nullptr};
+  if (ipos) {  // partitioned order: blocks claim tiles in order (see TileSched)
+    static const int grid = resident_grid(join_insert_kernel, kBuildThreads, 0);
+    gb = std::min(gb, grid);
+    CK(g.work_ctr.ensure(8));
+    CK(cudaMemsetAsync(g.work_ctr.p, 0, 8, s));
+    sched.ctr = g.work_ctr.as<unsigned long long>();
+  }
+  join_insert_kernel<<<gb, kBuildThreads, 0, s>>>(ikeys, ipos, nb, table, g.jmask, ga, sched);
   CKL();
   join_finalize_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, brows, ga, cap * kInline);
   CKL();
@@ -673,31 +785,56 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
   sc.off = g.sc_off.as<uint32_t>();
   sc.cnt = g.sc_cnt.as<uint32_t>();
   unsigned long long* tmp = g.totals2.as<unsigned long long>();
-  for (uint64_t c0 = 0; c0 < np; c0 += kSub) {
-    const uint64_t cn = std::min(kSub, np - c0);
-    const uint64_t nwt = (cn + kWarpTile - 1) / kWarpTile;
-    // one contiguous run of tiles per warp; enough warps to fill the GPU
-    const uint64_t want_warps = std::min<uint64_t>(nwarps_max, nwt);
-    const uint64_t per_warp = (nwt + want_warps - 1) / want_warps;
-    const uint64_t warps = (nwt + per_warp - 1) / per_warp;
-    const uint64_t blocks = (warps + kProbeWarps - 1) / kProbeWarps;
-    sc.wentries = g.wcount.as<uint32_t>();
-    sc.wpairs = sc.wentries + blocks * kProbeWarps;
-    CK(g.partial.ensure(blocks * 8));
-    unsigned long long* part = g.partial.as<unsigned long long>();
-    join_match_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(pkeys + c0, prows + c0, cn, g.table.as<Slot>(),
-                                                                 g.jmask, sc, nwt, per_warp, part,
-                                                                 g.jflags.as<unsigned int>());
-    CKL();
-    const bool last = c0 + kSub >= np;
-    const unsigned long long* bin = c0 == 0 ? base_in : tmp + ((c0 / kSub) & 1);
-    unsigned long long* bout = last ? total_out : tmp + (((c0 / kSub) + 1) & 1);
-    scan_partials_kernel<<<1, kScanThreads, 0, s>>>(part, (uint32_t)blocks, bin, bout);
-    CKL();
-    join_emit_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(sc, g.rows_arr.as<uint32_t>(), nwt, per_warp, part,
-                                                                out_p, out_b, cap);
-    CKL();
-    g_launches += 3;
+  // Partition the probe side (in spans of kSpan probes) when a span reuses each
+  // table slice several times: span * 32 B of slot-pair reads >= 2x the table.
+  constexpr uint64_t kSpan = 1ull << 30;
+  const uint64_t force = env_u64("GOLP_JOIN_PART_PROBE", 2);
+  const bool part_probe =
+      g.jparts > 1 && (force == 1 || (force == 2 && std::min(np, kSpan) >= g.jcap));
+  const uint64_t span = part_probe ? kSpan : np;
+  for (uint64_t s0 = 0; s0 < np; s0 += span) {
+    const uint64_t sn = std::min(span, np - s0);
+    if (part_probe) RET(probe_partitioned(pkeys + s0, sn, s));
+    for (uint64_t c0 = s0; c0 < s0 + sn; c0 += kSub) {
+      const uint64_t cn = std::min(kSub, s0 + sn - c0);
+      const uint64_t nwt = (cn + kWarpTile - 1) / kWarpTile;
+      // one contiguous run of tiles per warp; enough warps to fill the GPU
+      const uint64_t want_warps = std::min<uint64_t>(nwarps_max, nwt);
+      // the partitioned path runs one block per partition tile (kRunWarpTiles per warp)
+      const uint64_t per_warp = part_probe ? kRunWarpTiles : (nwt + want_warps - 1) / want_warps;
+      const uint64_t warps = (nwt + per_warp - 1) / per_warp;
+      const uint64_t blocks = (warps + kProbeWarps - 1) / kProbeWarps;
+      sc.wentries = g.wcount.as<uint32_t>();
+      sc.wpairs = sc.wentries + blocks * kProbeWarps;
+      CK(g.partial.ensure(blocks * 8));
+      unsigned long long* part = g.partial.as<unsigned long long>();
+      if (part_probe) {
+        const uint64_t tile0 = (c0 - s0) / kPartTile;  // sub-chunks start on partition tiles
+        static bool attr = false;
+        if (!attr) {
+          CK(cudaFuncSetAttribute(join_match_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunSmem));
+          attr = true;
+        }
+        join_match_runs_kernel<<<(unsigned)blocks, kProbeThreads, kRunSmem, s>>>(
+            prows + c0, cn, g.res_part.as<uint64_t>(), g.part_pos.as<uint16_t>(),
+            g.run_base.as<uint32_t>() + tile0 * g.jparts, g.run_len.as<uint16_t>() + tile0 * g.jparts, g.jparts, sc,
+            part);
+      } else {
+        join_match_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(pkeys + c0, prows + c0, cn, g.table.as<Slot>(),
+                                                                     g.jmask, sc, nwt, per_warp, part);
+      }
+      CKL();
+      const uint64_t ci = c0 / kSub;  // kSpan is a multiple of kSub
+      const bool last = c0 + cn >= np;
+      const unsigned long long* bin = c0 == 0 ? base_in : tmp + (ci & 1);
+      unsigned long long* bout = last ? total_out : tmp + ((ci + 1) & 1);
+      scan_partials_kernel<<<1, kScanThreads, 0, s>>>(part, (uint32_t)blocks, bin, bout);
+      CKL();
+      join_emit_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(sc, g.rows_arr.as<uint32_t>(), nwt, per_warp,
+                                                                  part, out_p, out_b, cap);
+      CKL();
+      g_launches += 3;
+    }
   }
   return GOLP_OK;
 }
@@ -710,20 +847,8 @@ int read_u64(const void* dptr, uint64_t* out, cudaStream_t s) {
   return GOLP_OK;
 }
 
-// Match count of a finished probe + the kernels' overflow flag (one sync).
-int read_probe_total(const void* dptr, uint64_t* out, cudaStream_t s) {
-  uint64_t* h = static_cast<uint64_t*>(g.pin_small);
-  CK(cudaMemcpyAsync(h, dptr, 8, cudaMemcpyDeviceToHost, s));
-  if (g.jflags.p) CK(cudaMemcpyAsync(h + 1, g.jflags.p, 4, cudaMemcpyDeviceToHost, s));
-  else h[1] = 0;
-  CK(cudaStreamSynchronize(s));
-  *out = h[0];
-  if (g.jflags.p && (uint32_t)h[1] != 0) {
-    set_error("a build key occurs more than 2^24-1 times; the packed probe entry cannot describe it");
-    return GOLP_ERR_CAPACITY;
-  }
-  return GOLP_OK;
-}
+// Match count of a finished probe (one sync).
+int read_probe_total(const void* dptr, uint64_t* out, cudaStream_t s) { return read_u64(dptr, out, s); }
 
 int join_probe_impl(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
                     uint64_t cap, uint64_t* out_m, cudaStream_t s) {
@@ -771,7 +896,7 @@ int golp_shutdown(void) {
   g.pool.stop();
   DevBuf* bufs[] = {&g.ctl, &g.cand_hi, &g.cand_lo, &g.w_hi, &g.w_lo, &g.out_rows, &g.out_hi, &g.samples,
                     &g.table, &g.rows_arr, &g.ovf, &g.big_list, &g.jcount,
-                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.jflags, &g.pairs_p, &g.pairs_b, &g.in_keys, &g.in_rows,
+                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.in_keys, &g.in_rows,
                     &g.in_bkeys, &g.in_brows, &g.in_payload};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < kSlots; ++i) {
@@ -868,7 +993,6 @@ int golp_join_build_device(const double* d_build_keys, const uint32_t* d_build_r
   cudaStream_t s = as_stream(stream);
   RET(join_build_impl(d_build_keys, d_build_rows, nb, s));
   g.build_timed = g.prof;  // resolved lazily by golp_last_kernel_times (no sync here)
-  g.kt.join_capacity = g.jcap;
   return GOLP_OK;
 }
 
@@ -1129,9 +1253,7 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
       }
       RET(launch_probe(dpk + c0, dpr + c0, cn, op, ob, cap_, totals + c, totals + c + 1, s));
       publish_u64_kernel<<<1, 1, 0, s>>>(reinterpret_cast<volatile unsigned long long*>(g.mirror_dev + c + 1),
-                                         totals + c + 1,
-                                         reinterpret_cast<volatile unsigned int*>(g.mirror_dev + nchunks + 1),
-                                         g.jflags.as<unsigned int>());
+                                         totals + c + 1);
       CKL();
       ++g_launches;
       CK(cudaEventRecord(g.chunk_ev[c], s));
@@ -1139,7 +1261,6 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
     }
     return GOLP_OK;
   };
-  g.mirror[nchunks + 1] = 0;
   RET(run_chunks(true, dev_p, dev_b, dcap));
   if (trace) std::fprintf(stderr, "[golp] %.3f ms all chunks queued\n", (wall_seconds() - t0) * 1e3);
   CK(cudaEventRecord(ev_chunk, g.s_h2d));
@@ -1160,10 +1281,6 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
     if (nchunks) {
       CK(cudaEventSynchronize(g.chunk_ev[nchunks - 1]));
       *m_out = g.mirror[nchunks];
-      if ((uint32_t)g.mirror[nchunks + 1] != 0) {
-        set_error("a build key occurs more than 2^24-1 times; the packed probe entry cannot describe it");
-        return GOLP_ERR_CAPACITY;
-      }
     } else {
       CK(cudaStreamSynchronize(s));
       *m_out = 0;

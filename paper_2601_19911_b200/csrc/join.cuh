@@ -35,6 +35,11 @@ struct __align__(16) Slot {
 __host__ __device__ __forceinline__ uint64_t home_slot(uint64_t bits, uint64_t mask) {
   return mix64(bits) & mask & ~1ull;
 }
+// Same for a 32-bit mask (tables are at most 2^32 slots).
+__host__ __device__ __forceinline__ uint32_t home_slot32(uint64_t bits, uint32_t mask) {
+  return (uint32_t)mix64(bits) & mask & ~1u;
+}
+
 
 // Key groups: the first kInline build positions of every group are recorded in
 // a slot-indexed side array while inserting (rows[h*kInline + rank]); one pass
@@ -45,6 +50,7 @@ __host__ __device__ __forceinline__ uint64_t home_slot(uint64_t bits, uint64_t m
 //                   rank >= kInline come from an overflow list; one block sorts
 // so no per-entry slot/rank arrays and no offset/fill/sort chain are needed for
 // the common (small) groups. Probe: cnt >= 2 reads rows[off + m].
+
 constexpr uint32_t kInline = 4;
 constexpr uint32_t kGroupTile = 16384;  // big groups up to this size sorted in shared memory (64 KB)
 
@@ -71,9 +77,35 @@ struct GroupArrays {
   uint32_t* big_list;  // big groups, then (appended) the ones above kThreadGroup
 };
 
-__global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double* __restrict__ bkeys, uint64_t nb,
-                                                                    Slot* table, uint64_t mask, GroupArrays ga) {
-  for (uint64_t t0 = (uint64_t)blockIdx.x * kBuildTile; t0 < nb; t0 += (uint64_t)gridDim.x * kBuildTile) {
+// Tile schedule of kernels that walk slice-partitioned entries: with a counter,
+// blocks claim tiles in order, so the tiles in flight stay consecutive (and in
+// one or two table slices) however unevenly the SMs progress; without one, a
+// plain grid-stride loop.
+struct TileSched {
+  unsigned long long* ctr;
+  __device__ __forceinline__ uint64_t first(unsigned long long* s_t) const {
+    return ctr ? claim(s_t) : blockIdx.x;
+  }
+  __device__ __forceinline__ uint64_t next(uint64_t t, unsigned long long* s_t) const {
+    return ctr ? claim(s_t) : t + gridDim.x;
+  }
+  __device__ __forceinline__ uint64_t claim(unsigned long long* s_t) const {
+    __syncthreads();  // all threads have read the previous claim
+    if (threadIdx.x == 0) *s_t = atomicAdd(ctr, 1ull);
+    __syncthreads();
+    return *s_t;
+  }
+};
+
+// bpos (optional): build position of entry i when the entries were partitioned.
+__global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double* __restrict__ bkeys,
+                                                                    const uint32_t* __restrict__ bpos, uint64_t nb,
+                                                                    Slot* table, uint64_t mask, GroupArrays ga,
+                                                                    TileSched sched) {
+  __shared__ unsigned long long s_t;
+  const uint64_t ntiles = (nb + kBuildTile - 1) / kBuildTile;
+  for (uint64_t t = sched.first(&s_t); t < ntiles; t = sched.next(t, &s_t)) {
+    const uint64_t t0 = t * kBuildTile;
     uint64_t b[kBuildItems];
     uint32_t h[kBuildItems];
     unsigned pending = 0;
@@ -108,13 +140,14 @@ __global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double
     for (int j = 0; j < kBuildItems; ++j) {
       const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
       const bool ok = (valid >> j) & 1u;
-      if (ok && r[j] < kInline) ga.rows[(uint64_t)h[j] * kInline + r[j]] = (uint32_t)i;
+      const uint32_t pos = ok ? (bpos ? __ldg(bpos + i) : (uint32_t)i) : 0u;
+      if (ok && r[j] < kInline) ga.rows[(uint64_t)h[j] * kInline + r[j]] = pos;
       const bool ovf = ok && r[j] >= kInline;
       const unsigned long long k = warp_append(&ga.counters[0], ovf);
       if (ovf) {
         ga.ovf_slot[k] = h[j];
         ga.ovf_rank[k] = r[j];
-        ga.ovf_pos[k] = (uint32_t)i;
+        ga.ovf_pos[k] = pos;
       }
     }
   }
@@ -260,13 +293,17 @@ constexpr int kWarpItems = GOLP_WARP_ITEMS;
 static_assert(kWarpItems % 2 == 0, "keys are loaded as 16-byte pairs");
 constexpr uint32_t kWarpTile = 32 * kWarpItems;  // probes per warp tile
 constexpr int kProbeThreads = 256;
-constexpr uint32_t kMaxGroup = (1u << 24) - 1;  // largest key group an entry can describe
 
 // L2 eviction policies: the table should survive the probe stream in L2, the
 // streamed probe columns should not displace it.
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -288,6 +325,16 @@ __device__ __forceinline__ double2 ldg_stream_d2(const double* p, uint64_t pol) 
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
                : "=d"(r.x), "=d"(r.y)
                : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ldg_stream_f64(const double* p, uint64_t pol) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint64_t ldg_stream_u64(const uint64_t* p, uint64_t pol) {
+  uint64_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
   return r;
 }
 __device__ __forceinline__ uint4 ldg_stream_u4(const uint32_t* p, uint64_t pol) {
@@ -347,6 +394,188 @@ __global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(unsigned lo
   if (threadIdx.x == 0) *total_out = carry;
 }
 
+// ---- radix partitioning (tables larger than ~L2/2) ----------------------------------
+// The table is viewed as P slices of 2^slice_bits slots; a key's slice is the
+// top bits of its home slot. Processing entries slice by slice keeps the part of
+// the table being walked L2-resident. This is only a schedule: the walks are the
+// ordinary table-wide linear probes (one that runs off the end of its slice just
+// touches the next one), so the table is the same as an unpartitioned build and
+// skewed keys cannot overfill a slice.
+//
+// Entries are grouped by slice with a count pass, a scan of the P totals and a
+// scatter that sorts each tile of kPartTile entries by slice in shared memory and
+// writes every slice's run of the tile contiguously at a reserved offset. The
+// order inside a partition does not matter: the build inserts in any order and
+// sorts key groups by position afterwards; the probe records each entry's index
+// inside its tile plus the (offset, length) of every (tile, slice) run, so
+// join_unpartition_kernel can put results back in probe order tile by tile with
+// coalesced reads and writes (no scattered 8-byte stores).
+constexpr int kPartThreads = 512;
+constexpr int kPartItems = 8;
+constexpr uint32_t kPartTile = (uint32_t)kPartThreads * kPartItems;  // 4096 entries
+constexpr uint32_t kMaxParts = 1024;
+constexpr uint32_t kMaxProbeParts = 256;  // bounds the per-(tile, slice) run table
+constexpr size_t kPartSmem = (size_t)kPartTile * (8 + 2 + 2) + (size_t)kMaxParts * (4 + 4 + 8);
+
+__device__ __forceinline__ uint32_t part_of(double k, uint32_t mask, int slice_bits) {
+  return home_slot32(canon_bits(k), mask) >> slice_bits;
+}
+
+__global__ void __launch_bounds__(kPartThreads) part_count_kernel(const double* __restrict__ keys, uint64_t n,
+                                                                  uint32_t mask, int slice_bits, uint32_t nparts,
+                                                                  unsigned long long* __restrict__ counts) {
+  __shared__ unsigned s_h[kMaxParts];
+  for (uint32_t p = threadIdx.x; p < nparts; p += blockDim.x) s_h[p] = 0;
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  const uint64_t n2 = n / 2;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n2; i += 4 * stride) {  // 4 independent 16-byte loads in flight
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = ldg_stream_d2(keys + 2 * (i + u * stride), pol);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      atomicAdd(&s_h[part_of(v[u].x, mask, slice_bits)], 1u);
+      atomicAdd(&s_h[part_of(v[u].y, mask, slice_bits)], 1u);
+    }
+  }
+  for (; i < n2; i += stride) {
+    const double2 v = ldg_stream_d2(keys + 2 * i, pol);
+    atomicAdd(&s_h[part_of(v.x, mask, slice_bits)], 1u);
+    atomicAdd(&s_h[part_of(v.y, mask, slice_bits)], 1u);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&s_h[part_of(keys[n - 1], mask, slice_bits)], 1u);
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < nparts; p += blockDim.x)
+    if (s_h[p]) atomicAdd(&counts[p], (unsigned long long)s_h[p]);
+}
+
+// counts -> exclusive offsets written to cursors (one block).
+__global__ void __launch_bounds__(1024) part_scan_kernel(const unsigned long long* __restrict__ counts,
+                                                         unsigned long long* __restrict__ cursors, uint32_t nparts) {
+  __shared__ unsigned long long s_w[33];
+  unsigned long long carry = 0;
+  for (uint32_t b0 = 0; b0 < nparts; b0 += blockDim.x) {
+    const uint32_t i = b0 + threadIdx.x;
+    const unsigned long long v = i < nparts ? counts[i] : 0ull;
+    unsigned long long tot;
+    const unsigned long long e = block_excl_scan(v, s_w, &tot);
+    if (i < nparts) cursors[i] = carry + e;
+    carry += tot;
+  }
+}
+
+struct PartOut {
+  double* keys;        // entries grouped by slice
+  uint32_t* pos;       // build side: the entry's position (or null)
+  uint16_t* idx;       // probe side: the entry's index inside its tile (or null)
+  uint32_t* run_base;  // probe side: [tile * nparts + p] = offset of the tile's run of slice p
+  uint16_t* run_len;   //             and its length
+};
+
+// Exclusive scan of s_cnt[0..nparts) into s_start (nparts <= 2 * blockDim.x).
+__device__ __forceinline__ void block_scan_parts(const unsigned* s_cnt, unsigned* s_start, uint32_t nparts,
+                                                 unsigned long long* s_w) {
+  const uint32_t i0 = 2 * threadIdx.x;
+  const unsigned a = i0 < nparts ? s_cnt[i0] : 0u, b = i0 + 1 < nparts ? s_cnt[i0 + 1] : 0u;
+  unsigned long long tot;
+  const unsigned e = (unsigned)block_excl_scan((unsigned long long)(a + b), s_w, &tot);
+  if (i0 < nparts) s_start[i0] = e;
+  if (i0 + 1 < nparts) s_start[i0 + 1] = e + a;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(const double* __restrict__ keys, uint64_t n,
+                                                                    uint32_t mask, int slice_bits, uint32_t nparts,
+                                                                    unsigned long long* __restrict__ cursors,
+                                                                    PartOut out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* s_key = reinterpret_cast<double*>(smem);
+  uint16_t* s_loc = reinterpret_cast<uint16_t*>(s_key + kPartTile);
+  uint16_t* s_part = s_loc + kPartTile;
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_part + kPartTile);
+  unsigned* s_start = s_cnt + kMaxParts;
+  unsigned long long* s_base = reinterpret_cast<unsigned long long*>(s_start + kMaxParts);
+  __shared__ unsigned long long s_w[33];
+  const uint64_t pol = policy_evict_first();
+  const uint64_t ntiles = (n + kPartTile - 1) / kPartTile;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t t0 = t * kPartTile;
+    const uint32_t cnt = (uint32_t)(n - t0 < kPartTile ? n - t0 : kPartTile);
+    for (uint32_t p = threadIdx.x; p < nparts; p += blockDim.x) s_cnt[p] = 0;
+    __syncthreads();
+    double k[kPartItems];
+    uint32_t pr[kPartItems];  // part << 16 | rank inside the tile's run
+    if (cnt == kPartTile && ((reinterpret_cast<uintptr_t>(keys + t0) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < kPartItems; j += 2) {
+        const double2 v = ldg_stream_d2(keys + t0 + 2 * threadIdx.x + (uint64_t)j * kPartThreads, pol);
+        k[j] = v.x;
+        k[j + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPartItems; j += 2) {
+        const uint32_t l = 2 * threadIdx.x + j * kPartThreads;
+        k[j] = l < cnt ? keys[t0 + l] : 0.0;
+        k[j + 1] = l + 1 < cnt ? keys[t0 + l + 1] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kPartItems; ++j) {
+      const uint32_t l = 2 * threadIdx.x + (j & ~1) * kPartThreads + (j & 1);
+      if (l < cnt) {
+        const uint32_t p = part_of(k[j], mask, slice_bits);
+        pr[j] = (p << 16) | atomicAdd(&s_cnt[p], 1u);
+      }
+    }
+    __syncthreads();
+    block_scan_parts(s_cnt, s_start, nparts, s_w);
+    for (uint32_t p = threadIdx.x; p < nparts; p += blockDim.x) {
+      const unsigned c = s_cnt[p];
+      const unsigned long long b = c ? atomicAdd(&cursors[p], (unsigned long long)c) : 0ull;
+      s_base[p] = b;
+      if (out.run_base) {
+        out.run_base[t * nparts + p] = (uint32_t)b;
+        out.run_len[t * nparts + p] = (uint16_t)c;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kPartItems; ++j) {
+      const uint32_t l = 2 * threadIdx.x + (j & ~1) * kPartThreads + (j & 1);
+      if (l < cnt) {
+        const uint32_t p = pr[j] >> 16;
+        const uint32_t d = s_start[p] + (pr[j] & 0xFFFFu);
+        s_key[d] = k[j];
+        s_loc[d] = (uint16_t)l;
+        s_part[d] = (uint16_t)p;
+      }
+    }
+    __syncthreads();
+    uint32_t o[kPartItems];  // destinations (entry counts are < 2^32)
+#pragma unroll
+    for (int u = 0; u < kPartItems; ++u) {  // resolve all destinations first (independent smem loads)
+      const uint32_t i = threadIdx.x + u * kPartThreads;
+      if (i < cnt) {
+        const uint32_t p = s_part[i];
+        o[u] = (uint32_t)s_base[p] + (i - s_start[p]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kPartItems; ++u) {
+      const uint32_t i = threadIdx.x + u * kPartThreads;
+      if (i < cnt) {
+        out.keys[o[u]] = s_key[i];
+        if (out.pos) out.pos[o[u]] = (uint32_t)(t0 + s_loc[i]);
+        if (out.idx) out.idx[o[u]] = s_loc[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ void st_hint(uint32_t* p, uint32_t v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
 }
@@ -373,22 +602,77 @@ struct MatchScratch {
 
 constexpr unsigned kProbeWarps = kProbeThreads / 32;
 
+// Appends one warp tile's hits (probe row, slot.off, slot.cnt) to the warp's
+// scratch run in probe order; returns the tile's pair count.
+__device__ __forceinline__ uint32_t warp_append_hits(unsigned lane, uint64_t first, const uint32_t* off,
+                                                     const uint32_t* cnt, const uint32_t* __restrict__ prows,
+                                                     const MatchScratch& sc, uint64_t& cursor) {
+  uint32_t nm = 0, npr = 0;
+#pragma unroll
+  for (int j = 0; j < kWarpItems; ++j) {
+    nm += cnt[j] != 0;
+    npr += cnt[j];
+  }
+  uint32_t incl = nm;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if ((int)lane >= o) incl += v;
+  }
+  uint32_t tpairs = npr;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tpairs += __shfl_xor_sync(0xFFFFFFFFu, tpairs, o);
+  const uint32_t tmatch = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  if (nm) {
+    uint32_t r[kWarpItems];
+#pragma unroll
+    for (int j = 0; j < kWarpItems; ++j) r[j] = cnt[j] ? __ldg(prows + first + j) : 0u;
+    uint64_t o = cursor + (incl - nm);
+#pragma unroll
+    for (int j = 0; j < kWarpItems; ++j) {
+      if (cnt[j]) {
+        sc.prow[o] = r[j];
+        sc.off[o] = off[j];
+        sc.cnt[o] = cnt[j];
+        ++o;
+      }
+    }
+  }
+  cursor += tmatch;
+  return tpairs;
+}
+
+// Per-warp totals -> scratch counters and the block's pair total.
+__device__ __forceinline__ void finish_match_block(unsigned lane, unsigned warp, uint64_t gw, uint64_t lo,
+                                                   uint64_t cursor, uint64_t pairs_total, const MatchScratch& sc,
+                                                   unsigned long long* s_w, unsigned long long* __restrict__ bpart) {
+  if (lane == 0) {
+    sc.wentries[gw] = (uint32_t)(cursor - lo * kWarpTile);
+    sc.wpairs[gw] = (uint32_t)pairs_total;
+    s_w[warp] = pairs_total;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (unsigned w = 0; w < kProbeWarps; ++w) t += s_w[w];
+    bpart[blockIdx.x] = t;
+  }
+}
+
 __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_kernel(
     const double* __restrict__ pkeys, const uint32_t* __restrict__ prows, uint64_t np, const Slot* __restrict__ table,
-    uint64_t mask, MatchScratch sc, uint64_t nwt, uint64_t per_warp, unsigned long long* __restrict__ bpart,
-    unsigned int* __restrict__ flags) {
+    uint64_t mask, MatchScratch sc, uint64_t nwt, uint64_t per_warp, unsigned long long* __restrict__ bpart) {
   __shared__ unsigned long long s_w[kProbeWarps];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint64_t pol_stream = policy_evict_first(), pol_table = policy_evict_last();
   const uint64_t gw = (uint64_t)blockIdx.x * kProbeWarps + warp;
   const uint64_t lo = gw * per_warp, hi = lo + per_warp < nwt ? lo + per_warp : nwt;
-  const uint32_t pm = (uint32_t)mask;
   uint64_t cursor = lo * kWarpTile;  // next free scratch entry of this warp
   uint64_t pairs_total = 0;
   for (uint64_t wt = lo; wt < hi; ++wt) {
     const uint64_t first = wt * kWarpTile + lane * kWarpItems;
+    uint32_t off[kWarpItems], cnt[kWarpItems];
     double k[kWarpItems];
-    uint32_t r[kWarpItems];
     if (first + kWarpItems <= np && (((uintptr_t)(pkeys + first) & 15) == 0)) {
 #pragma unroll
       for (int j = 0; j < kWarpItems; j += 2) {
@@ -401,12 +685,12 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_ker
       for (int j = 0; j < kWarpItems; ++j) k[j] = first + j < np ? pkeys[first + j] : 0.0;
     }
     uint64_t bits[kWarpItems];
-    uint32_t h[kWarpItems], off[kWarpItems], cnt[kWarpItems];
+    uint32_t h[kWarpItems];
     unsigned pending = 0;
 #pragma unroll
     for (int j = 0; j < kWarpItems; ++j) {
       bits[j] = canon_bits(k[j]);
-      h[j] = (uint32_t)home_slot(bits[j], mask);
+      h[j] = home_slot32(bits[j], (uint32_t)mask);
       off[j] = 0;
       cnt[j] = 0;
       if (first + j < np) pending |= 1u << j;
@@ -421,54 +705,151 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_ker
         if (!(pending & (1u << j))) continue;
         const int st = check_pair(sl[j], bits[j], off[j], cnt[j]);
         if (st >= 0) pending &= ~(1u << j);
-        else h[j] = (h[j] + 2) & pm;
+        else h[j] = (h[j] + 2) & (uint32_t)mask;
       }
     }
-    uint32_t nm = 0, npr = 0;
+    pairs_total += warp_append_hits(lane, first, off, cnt, prows, sc, cursor);
+  }
+  finish_match_block(lane, warp, gw, lo, cursor, pairs_total, sc, s_w, bpart);
+}
+
+// Radix-partitioned probe: keys arrive grouped by table slice, so consecutive
+// threads walk the same L2-resident slice. res_part[i] = {off | cnt << 32} of the
+// slot of keys[i] (0 when absent), in partitioned order. Blocks claim chunks of
+// kPartProbeSub sub-tiles in order (TileSched); inside a chunk the keys of the
+// next sub-tile are loaded while the current one's lookups are in flight.
+constexpr int kPartProbeItems = 4;
+constexpr int kPartProbeSub = 8;
+__global__ void __launch_bounds__(kProbeThreads, 3) join_probe_part_kernel(const double* __restrict__ keys, uint64_t n,
+                                                                        const Slot* __restrict__ table, uint64_t mask,
+                                                                        uint64_t* __restrict__ res_part,
+                                                                        int table_policy, TileSched sched) {
+  __shared__ unsigned long long s_t;
+  const uint64_t pol_table = table_policy ? policy_evict_normal() : policy_evict_last();
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t sub = (uint64_t)kProbeThreads * kPartProbeItems;
+  const uint64_t chunk = sub * kPartProbeSub;
+  const uint64_t nchunks = (n + chunk - 1) / chunk;
+  for (uint64_t c = sched.first(&s_t); c < nchunks; c = sched.next(c, &s_t)) {
+    const uint64_t c0 = c * chunk + threadIdx.x;
+    double kc[kPartProbeItems];
 #pragma unroll
-    for (int j = 0; j < kWarpItems; ++j) {
-      nm += cnt[j] != 0;
-      npr += cnt[j];
+    for (int j = 0; j < kPartProbeItems; ++j) {
+      const uint64_t i = c0 + (uint64_t)j * kProbeThreads;
+      kc[j] = i < n ? ldg_stream_f64(keys + i, pol_stream) : 0.0;
     }
-    uint32_t incl = nm;
+    for (int u = 0; u < kPartProbeSub; ++u) {
+      const uint64_t base = c0 + (uint64_t)u * sub;
+      if (base - threadIdx.x >= n) break;
+      double kn[kPartProbeItems];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if ((int)lane >= o) incl += v;
-    }
-    uint32_t tpairs = npr;
+      for (int j = 0; j < kPartProbeItems; ++j) {
+        const uint64_t i = base + sub + (uint64_t)j * kProbeThreads;
+        kn[j] = (u + 1 < kPartProbeSub && i < n) ? ldg_stream_f64(keys + i, pol_stream) : 0.0;
+      }
+      uint64_t bits[kPartProbeItems];
+      uint32_t h[kPartProbeItems], off[kPartProbeItems], cnt[kPartProbeItems];
+      unsigned pending = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tpairs += __shfl_xor_sync(0xFFFFFFFFu, tpairs, o);
-    pairs_total += tpairs;
-    const uint32_t tmatch = __shfl_sync(0xFFFFFFFFu, incl, 31);
-    if (nm) {
+      for (int j = 0; j < kPartProbeItems; ++j) {
+        bits[j] = canon_bits(kc[j]);
+        h[j] = home_slot32(bits[j], (uint32_t)mask);
+        off[j] = 0;
+        cnt[j] = 0;
+        if (base + (uint64_t)j * kProbeThreads < n) pending |= 1u << j;
+      }
+      while (pending) {
+        ulonglong4 sl[kPartProbeItems];
 #pragma unroll
-      for (int j = 0; j < kWarpItems; ++j) r[j] = cnt[j] ? __ldg(prows + first + j) : 0u;
-      uint64_t o = cursor + (incl - nm);
+        for (int j = 0; j < kPartProbeItems; ++j)
+          if (pending & (1u << j)) sl[j] = ldg_pair(table + h[j], pol_table);
 #pragma unroll
-      for (int j = 0; j < kWarpItems; ++j) {
-        if (cnt[j]) {
-          sc.prow[o] = r[j];
-          sc.off[o] = off[j];
-          sc.cnt[o] = cnt[j];
-          ++o;
+        for (int j = 0; j < kPartProbeItems; ++j) {
+          if (!(pending & (1u << j))) continue;
+          const int st = check_pair(sl[j], bits[j], off[j], cnt[j]);
+          if (st >= 0) pending &= ~(1u << j);
+          else h[j] = (h[j] + 2) & (uint32_t)mask;
         }
       }
+#pragma unroll
+      for (int j = 0; j < kPartProbeItems; ++j) {
+        const uint64_t i = base + (uint64_t)j * kProbeThreads;
+        if (i < n) res_part[i] = ((uint64_t)cnt[j] << 32) | off[j];
+        kc[j] = kn[j];
+      }
     }
-    cursor += tmatch;
   }
-  if (lane == 0) {
-    sc.wentries[gw] = (uint32_t)(cursor - lo * kWarpTile);
-    sc.wpairs[gw] = (uint32_t)pairs_total;
-    s_w[warp] = pairs_total;
+}
+
+// Match stage of the radix-partitioned probe: block b owns partition tile b
+// (kPartTile probes). It gathers the tile's lookup results from its runs in
+// res_part (one contiguous run per slice) into shared memory at their recorded
+// in-tile indices, then its warps append hits exactly like join_match_kernel
+// with per_warp = kRunWarpTiles, so scan_partials/emit are shared.
+constexpr uint32_t kRunWarpTiles = kPartTile / (kProbeWarps * kWarpTile);
+static_assert(kRunWarpTiles * kProbeWarps * kWarpTile == kPartTile, "partition tile must split into warp tiles");
+constexpr size_t kRunSmem = (size_t)kPartTile * 8;
+
+__global__ void __launch_bounds__(kProbeThreads) join_match_runs_kernel(
+    const uint32_t* __restrict__ prows, uint64_t np, const uint64_t* __restrict__ res_part,
+    const uint16_t* __restrict__ idx, const uint32_t* __restrict__ run_base, const uint16_t* __restrict__ run_len,
+    uint32_t nparts, MatchScratch sc, unsigned long long* __restrict__ bpart) {
+  extern __shared__ __align__(16) uint64_t s_res[];  // kPartTile entries
+  __shared__ unsigned s_cnt[kMaxProbeParts], s_start[kMaxProbeParts], s_base[kMaxProbeParts];
+  __shared__ uint8_t s_pj[kPartTile];  // slice of the j-th entry of the tile's concatenated runs
+  __shared__ unsigned long long s_w[33];
+  static_assert(kMaxProbeParts <= 256, "s_pj stores slice ids as bytes");
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t pol = policy_evict_first();
+  const uint64_t t = blockIdx.x, t0 = t * kPartTile;
+  const uint32_t tcnt = (uint32_t)(np - t0 < kPartTile ? np - t0 : kPartTile);
+  for (uint32_t p = threadIdx.x; p < nparts; p += blockDim.x) {
+    s_cnt[p] = run_len[t * nparts + p];
+    s_base[p] = run_base[t * nparts + p];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (unsigned w = 0; w < kProbeWarps; ++w) t += s_w[w];
-    bpart[blockIdx.x] = t;
+  block_scan_parts(s_cnt, s_start, nparts, s_w);
+  for (uint32_t p = threadIdx.x; p < nparts; p += blockDim.x) {  // expand runs -> slice id per entry
+    const uint32_t b = s_start[p], e = b + s_cnt[p];
+    for (uint32_t j = b; j < e; ++j) s_pj[j] = (uint8_t)p;
   }
-  (void)flags;
+  __syncthreads();
+  constexpr int kBatch = 8;  // independent gathers in flight per thread
+  for (uint32_t j0 = threadIdx.x; j0 < tcnt; j0 += kBatch * kProbeThreads) {
+    uint64_t v[kBatch];
+    uint32_t d[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint32_t j = j0 + u * kProbeThreads;
+      if (j < tcnt) {
+        const uint32_t p = s_pj[j];
+        const uint64_t src = (uint64_t)s_base[p] + (j - s_start[p]);
+        d[u] = idx[src];
+        v[u] = ldg_stream_u64(res_part + src, pol);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (j0 + u * kProbeThreads < tcnt) s_res[d[u]] = v[u];
+  }
+  __syncthreads();
+  const uint64_t gw = t * kProbeWarps + warp;
+  const uint64_t nwt = (np + kWarpTile - 1) / kWarpTile;
+  const uint64_t lo = gw * kRunWarpTiles, hi = lo + kRunWarpTiles < nwt ? lo + kRunWarpTiles : nwt;
+  uint64_t cursor = lo * kWarpTile;
+  uint64_t pairs_total = 0;
+  for (uint64_t wt = lo; wt < hi; ++wt) {
+    const uint64_t first = wt * kWarpTile + lane * kWarpItems;
+    uint32_t off[kWarpItems], cnt[kWarpItems];
+#pragma unroll
+    for (int j = 0; j < kWarpItems; ++j) {
+      const uint64_t v = first + j < np ? s_res[first + j - t0] : 0ull;
+      off[j] = (uint32_t)v;
+      cnt[j] = (uint32_t)(v >> 32);
+    }
+    pairs_total += warp_append_hits(lane, first, off, cnt, prows, sc, cursor);
+  }
+  finish_match_block(lane, warp, gw, lo, cursor, pairs_total, sc, s_w, bpart);
 }
 
 // Same block/warp -> tile mapping as join_match_kernel. bpart holds the exclusive

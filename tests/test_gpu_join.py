@@ -98,3 +98,57 @@ def test_join_resident_api(cuda):
     small = torch.empty(10, dtype=torch.int32, device=cuda)
     with pytest.raises(CapacityError):
         resident.join_probe(t(pk), t(pr), small, small.clone())
+
+
+# ---- radix-partitioned join (tables larger than two slices) -------------------
+# GOLP_JOIN_SLICE_BYTES shrinks the slice so small builds take the partitioned
+# path; GOLP_JOIN_PART_PROBE=1 forces the slice-ordered probe as well.
+@pytest.mark.parametrize("slice_bytes", [64, 1024, 65536])
+@pytest.mark.parametrize("part_probe", ["0", "1"])
+@pytest.mark.parametrize("nb,np_,domain", [
+    (100_000, 1_000_000, 200_000),
+    (50_000, 300_000, 5_000),
+    (200_000, 100_000, 300),
+    (5000, 70_000, 1 << 40),
+])
+def test_partitioned_join_vs_oracle(b200, monkeypatch, slice_bytes, part_probe, nb, np_, domain):
+    from paper_2601_19911_b200 import _native
+
+    monkeypatch.setenv("GOLP_JOIN_SLICE_BYTES", str(slice_bytes))
+    monkeypatch.setenv("GOLP_JOIN_PART_PROBE", part_probe)
+    rng = np.random.default_rng(nb ^ np_ ^ slice_bytes)
+    bk = rng.integers(0, domain, size=nb).astype(np.float64)
+    pk = np.concatenate([rng.choice(bk, size=np_ // 2), rng.integers(0, domain, size=np_ - np_ // 2)])
+    rng.shuffle(pk)
+    br = rng.permutation(nb).astype(np.uint32)
+    pr = rng.permutation(np_).astype(np.uint32)
+    _native.check(_native.load().golp_set_profiling(1))
+    try:
+        res = b200.probe(KeyVector(bk, br), KeyVector(pk, pr))
+        kt = _native.kernel_times()
+    finally:
+        _native.check(_native.load().golp_set_profiling(0))
+    assert kt["join_slices"] > 1
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert np.array_equal(res.payload.probe_rows, ep)
+    assert np.array_equal(res.payload.build_rows, eb)
+
+
+def test_partitioned_join_resident_subchunks(cuda, monkeypatch):
+    import torch
+
+    from paper_2601_19911_b200 import resident
+
+    monkeypatch.setenv("GOLP_JOIN_SLICE_BYTES", "65536")
+    monkeypatch.setenv("GOLP_JOIN_PART_PROBE", "1")
+    rng = np.random.default_rng(5)
+    nb, np_ = 400_000, 3_000_000
+    bk = rng.integers(0, 800_000, size=nb).astype(np.float64)
+    pk = rng.integers(0, 800_000, size=np_).astype(np.float64)
+    br = rng.permutation(nb).astype(np.uint32)
+    pr = rng.permutation(np_).astype(np.uint32)
+    t = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(cuda)  # noqa: E731
+    op, ob = resident.join(t(bk), t(br), t(pk), t(pr))
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert np.array_equal(op.cpu().numpy().view(np.uint32), ep)
+    assert np.array_equal(ob.cpu().numpy().view(np.uint32), eb)
