@@ -735,13 +735,16 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   int gb = grid_for((nb + kBuildItems - 1) / kBuildItems, kBuildThreads, 8);
   TileSched sched{nullptr};
   if (ipos) {  // partitioned order: blocks claim tiles in order (see TileSched)
-    static const int grid = resident_grid(join_insert_kernel, kBuildThreads, 0);
+    static const int grid = resident_grid(join_insert_kernel<true>, kBuildThreads, 0);
     gb = std::min(gb, grid);
     CK(g.work_ctr.ensure(8));
     CK(cudaMemsetAsync(g.work_ctr.p, 0, 8, s));
     sched.ctr = g.work_ctr.as<unsigned long long>();
   }
-  join_insert_kernel<<<gb, kBuildThreads, 0, s>>>(ikeys, ipos, nb, table, g.jmask, ga, sched);
+  if (g.jparts > 1)  // table in HBM: one 16-byte CAS per new key
+    join_insert_kernel<true><<<gb, kBuildThreads, 0, s>>>(ikeys, ipos, nb, table, g.jmask, ga, sched);
+  else
+    join_insert_kernel<false><<<gb, kBuildThreads, 0, s>>>(ikeys, ipos, nb, table, g.jmask, ga, sched);
   CKL();
   join_finalize_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, brows, ga, cap * kInline);
   CKL();

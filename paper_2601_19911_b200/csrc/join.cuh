@@ -41,15 +41,33 @@ __host__ __device__ __forceinline__ uint32_t home_slot32(uint64_t bits, uint32_t
 }
 
 
-// Key groups: the first kInline build positions of every group are recorded in
-// a slot-indexed side array while inserting (rows[h*kInline + rank]); one pass
-// over the slots then finalizes each group:
+// Key groups. Inserting claims an empty slot with one 16-byte CAS that writes
+// {key, off = position, cnt = 1}, so a key's first member needs no second atomic
+// and no side-array write; later members take rank = atomicAdd(cnt) and record
+// ranks 1..kInline-1 in a slot-indexed side array (rows[h*kInline + rank]),
+// higher ranks in an overflow list. One pass over the slots then finalizes each
+// group:
 //   cnt == 1        slot.off = the build row (probe reads no side array)
-//   2..kInline      positions sorted in place and turned into rows; slot.off = h*kInline
+//   2..kInline      positions sorted and turned into rows at rows[h*kInline..]; slot.off = h*kInline
 //   > kInline       a CSR range [off, off+cnt) after the side array; members of
-//                   rank >= kInline come from an overflow list; one block sorts
+//                   rank >= kInline come from the overflow list; sorted afterwards
 // so no per-entry slot/rank arrays and no offset/fill/sort chain are needed for
 // the common (small) groups. Probe: cnt >= 2 reads rows[off + m].
+
+// 16-byte compare-and-swap (sm_90+): returns the slot's previous contents.
+__device__ __forceinline__ ulonglong2 cas128(void* addr, ulonglong2 cmp, ulonglong2 val) {
+  ulonglong2 old;
+  asm volatile(
+      "{\n\t.reg .b128 c, v, d;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.global.cas.b128 d, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(old.x), "=l"(old.y)
+      : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(addr)
+      : "memory");
+  return old;
+}
 
 constexpr uint32_t kInline = 4;
 constexpr uint32_t kGroupTile = 16384;  // big groups up to this size sorted in shared memory (64 KB)
@@ -98,6 +116,11 @@ struct TileSched {
 };
 
 // bpos (optional): build position of entry i when the entries were partitioned.
+// kWide: claim slots with the 16-byte CAS (saves the rank atomic of a key's first
+// member; pays off when the table lives in HBM). Otherwise a 64-bit key CAS plus
+// rank = atomicAdd(cnt) for every member, the rank-0 member storing its position
+// in slot.off -- cheaper when the atomics resolve in L2.
+template <bool kWide>
 __global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double* __restrict__ bkeys,
                                                                     const uint32_t* __restrict__ bpos, uint64_t nb,
                                                                     Slot* table, uint64_t mask, GroupArrays ga,
@@ -107,47 +130,74 @@ __global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double
   for (uint64_t t = sched.first(&s_t); t < ntiles; t = sched.next(t, &s_t)) {
     const uint64_t t0 = t * kBuildTile;
     uint64_t b[kBuildItems];
-    uint32_t h[kBuildItems];
+    uint32_t h[kBuildItems], pos[kBuildItems], r[kBuildItems];
     unsigned pending = 0;
 #pragma unroll
     for (int j = 0; j < kBuildItems; ++j) {
       const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
       b[j] = i < nb ? canon_bits(__ldg(bkeys + i)) : 0ull;
+      pos[j] = i < nb ? (bpos ? __ldg(bpos + i) : (uint32_t)i) : 0u;
       h[j] = (uint32_t)home_slot(b[j], mask);
+      r[j] = 0;
       if (i < nb) pending |= 1u << j;
     }
     const unsigned valid = pending;
-    // Claim or find each key's slot: CAS issued for every pending entry at once.
+    unsigned dup = 0;  // entries whose key already owns a slot: take a rank with atomicAdd
+    // Claim or find each key's slot: the CASes of all pending entries go out together.
     while (pending) {
-      unsigned long long old[kBuildItems];
+      if constexpr (kWide) {
+        ulonglong2 old[kBuildItems];
 #pragma unroll
-      for (int j = 0; j < kBuildItems; ++j)
-        if (pending & (1u << j))
-          old[j] = atomicCAS(reinterpret_cast<unsigned long long*>(&table[h[j]].key), kEmptyKey,
-                             (unsigned long long)b[j]);
+        for (int j = 0; j < kBuildItems; ++j)
+          if (pending & (1u << j))
+            old[j] = cas128(&table[h[j]], make_ulonglong2(kEmptyKey, 0ull),
+                            make_ulonglong2(b[j], (1ull << 32) | pos[j]));
 #pragma unroll
-      for (int j = 0; j < kBuildItems; ++j) {
-        if (!(pending & (1u << j))) continue;
-        if (old[j] == kEmptyKey || old[j] == b[j]) pending &= ~(1u << j);
-        else h[j] = (h[j] + 1) & (uint32_t)mask;
+        for (int j = 0; j < kBuildItems; ++j) {
+          if (!(pending & (1u << j))) continue;
+          if (old[j].x == kEmptyKey) {
+            pending &= ~(1u << j);  // claimed: rank 0, position stored inline
+          } else if (old[j].x == b[j]) {
+            pending &= ~(1u << j);
+            dup |= 1u << j;
+          } else {
+            h[j] = (h[j] + 1) & (uint32_t)mask;
+          }
+        }
+      } else {
+        unsigned long long old[kBuildItems];
+#pragma unroll
+        for (int j = 0; j < kBuildItems; ++j)
+          if (pending & (1u << j))
+            old[j] = atomicCAS(reinterpret_cast<unsigned long long*>(&table[h[j]].key), kEmptyKey,
+                               (unsigned long long)b[j]);
+#pragma unroll
+        for (int j = 0; j < kBuildItems; ++j) {
+          if (!(pending & (1u << j))) continue;
+          if (old[j] == kEmptyKey || old[j] == b[j]) pending &= ~(1u << j);
+          else h[j] = (h[j] + 1) & (uint32_t)mask;
+        }
+        dup = valid;
       }
     }
-    uint32_t r[kBuildItems];
 #pragma unroll
     for (int j = 0; j < kBuildItems; ++j)
-      if (valid & (1u << j)) r[j] = atomicAdd(&table[h[j]].cnt, 1u);
+      if (dup & (1u << j)) r[j] = atomicAdd(&table[h[j]].cnt, 1u);
+    if constexpr (!kWide) {
+#pragma unroll
+      for (int j = 0; j < kBuildItems; ++j)
+        if ((dup & (1u << j)) && r[j] == 0) table[h[j]].off = pos[j];
+    }
 #pragma unroll
     for (int j = 0; j < kBuildItems; ++j) {
-      const uint64_t i = t0 + (uint64_t)j * kBuildThreads + threadIdx.x;
-      const bool ok = (valid >> j) & 1u;
-      const uint32_t pos = ok ? (bpos ? __ldg(bpos + i) : (uint32_t)i) : 0u;
-      if (ok && r[j] < kInline) ga.rows[(uint64_t)h[j] * kInline + r[j]] = pos;
+      const bool ok = ((dup >> j) & 1u) && r[j] > 0;  // rank 0 lives in slot.off
+      if (ok && r[j] < kInline) ga.rows[(uint64_t)h[j] * kInline + r[j]] = pos[j];
       const bool ovf = ok && r[j] >= kInline;
       const unsigned long long k = warp_append(&ga.counters[0], ovf);
       if (ovf) {
         ga.ovf_slot[k] = h[j];
         ga.ovf_rank[k] = r[j];
-        ga.ovf_pos[k] = pos;
+        ga.ovf_pos[k] = pos[j];
       }
     }
   }
@@ -167,17 +217,20 @@ __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t wb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; wb < cap; wb += stride) {
     const uint64_t h = wb + lane;
-    uint32_t cnt = 0;
+    uint32_t cnt = 0, first = 0;  // first: rank-0 position, stored inline by the claiming CAS
     if (h < cap) {
       const ulonglong2 sl = reinterpret_cast<const ulonglong2*>(table)[h];
-      if (sl.x != kEmptyKey) cnt = (uint32_t)(sl.y >> 32);
+      if (sl.x != kEmptyKey) {
+        cnt = (uint32_t)(sl.y >> 32);
+        first = (uint32_t)sl.y;
+      }
     }
     uint32_t* grp = ga.rows + h * kInline;
     if (cnt == 1) {
-      table[h].off = __ldg(brows + grp[0]);
+      table[h].off = __ldg(brows + first);
     } else if (cnt >= 2 && cnt <= kInline) {
       const uint4 v = *reinterpret_cast<const uint4*>(grp);
-      uint32_t p0 = v.x, p1 = v.y, p2 = cnt > 2 ? v.z : 0xFFFFFFFFu, p3 = cnt > 3 ? v.w : 0xFFFFFFFFu;
+      uint32_t p0 = first, p1 = v.y, p2 = cnt > 2 ? v.z : 0xFFFFFFFFu, p3 = cnt > 3 ? v.w : 0xFFFFFFFFu;
       cswap_u32(p0, p1); cswap_u32(p2, p3); cswap_u32(p0, p2); cswap_u32(p1, p3); cswap_u32(p1, p2);
       uint4 o;
       o.x = __ldg(brows + p0);
@@ -200,8 +253,8 @@ __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_
     if (need) {
       const uint64_t off = csr_base + base + incl - need;
       table[h].off = (uint32_t)off;
-      const uint4 v = *reinterpret_cast<const uint4*>(grp);  // ranks 0..3
-      ga.rows[off] = v.x;
+      const uint4 v = *reinterpret_cast<const uint4*>(grp);  // ranks 1..3
+      ga.rows[off] = first;
       ga.rows[off + 1] = v.y;
       ga.rows[off + 2] = v.z;
       ga.rows[off + 3] = v.w;
