@@ -123,6 +123,8 @@ struct Ctx {
   bool prof = false;
   bool build_timed = false;
   bool probe_timed = false;
+  bool topk_pending = false;  // fused Top-K in flight: candidates/fallback read on demand
+  bool topk_timed = false;
   golp_kernel_times kt{};
 };
 
@@ -166,6 +168,16 @@ int do_init(int device, uint64_t chunk_bytes, int host_threads) {
 int ensure_init() { return g.ready ? GOLP_OK : do_init(-1, 0, 0); }
 
 SelectCtl* ctl(int i) { return g.ctl.as<SelectCtl>() + i; }
+
+// Integer tuning knob from the environment (default when unset or malformed).
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  char* end = nullptr;
+  const unsigned long long x = strtoull(v, &end, 0);
+  return (end && *end == 0) ? (uint64_t)x : dflt;
+}
+
 
 // True when `p` lies in page-locked host memory (cudaHostAlloc'd, our result
 // arena, or a cudaHostRegister'ed caller buffer): the DMA engine can use it directly.
@@ -402,6 +414,7 @@ struct TopkPlan {
   uint64_t s;       // samples
   uint64_t need_s;  // rank of the threshold sample (1-based)
   uint64_t cap;     // candidate capacity
+  uint64_t expect;  // expected candidates
 };
 
 // With S stratified samples and K' = min(k, n), the number X of samples that
@@ -409,7 +422,7 @@ struct TopkPlan {
 // rank r = lam + 6 sqrt(lam) + 7 (lam = S K'/n) makes P(X >= r), the only way the
 // filter can keep fewer than K' items, negligible; expected survivors ~ r n / S.
 TopkPlan plan_topk(uint64_t n, uint64_t kk) {
-  TopkPlan p{true, 0, 0, 0};
+  TopkPlan p{true, 0, 0, 0, 0};
   if (n <= kSortTile) return p;
   uint64_t s = n / 256;
   s = std::max<uint64_t>(2048, std::min<uint64_t>(s, 262144));
@@ -421,6 +434,7 @@ TopkPlan plan_topk(uint64_t n, uint64_t kk) {
   p.s = s;
   p.need_s = need_s;
   p.cap = std::min<uint64_t>(n, std::max<uint64_t>(4 * expect + 65536, 1u << 20));
+  p.expect = expect;
   return p;
 }
 
@@ -475,6 +489,21 @@ SelectArgs<Src> make_args(Src src, uint64_t n, uint64_t need, int mode, int c, u
   return a;
 }
 
+template <class Src>
+int launch_rank(const SelectArgs<Src>& a, unsigned long long* clear_count, cudaStream_t s) {
+  static int blocks = 0;
+  if (!blocks) {
+    CK(cudaFuncSetAttribute(rank_select_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRankSmem));
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rank_select_kernel<Src>, kRankThreads, kRankSmem));
+    blocks = std::max(1, per) * g.sms;
+  }
+  rank_select_kernel<Src><<<blocks, kRankThreads, kRankSmem, s>>>(a, clear_count);
+  CKL();
+  ++g_launches;
+  return GOLP_OK;
+}
+
 int ensure_topk_ws(uint64_t kk, uint64_t cap) {
   CK(g.w_hi.ensure(std::max<uint64_t>(kk, 1) * 8));
   CK(g.w_lo.ensure(std::max<uint64_t>(kk, 1) * 4));
@@ -517,9 +546,11 @@ int ensure_status_words() {
   return GOLP_OK;
 }
 
-int read_topk_status(cudaStream_t s, int* bad, uint64_t* cands) {
+// status: 0 ok, 1 candidate set unusable (direct fallback), 2 too many
+// candidates for the rank kernel (grid engine over the same candidates).
+int read_topk_status(cudaStream_t s, int* status, uint64_t* cands) {
   CK(cudaStreamSynchronize(s));
-  *bad = *reinterpret_cast<volatile int*>(g.status_host) != 0;
+  *status = *reinterpret_cast<volatile int*>(g.status_host);
   *cands = *reinterpret_cast<volatile unsigned long long*>(g.status_host + 8);
   return GOLP_OK;
 }
@@ -552,6 +583,7 @@ int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint6
   RET(ensure_topk_ws(kk, p.direct ? 0 : p.cap));
   g.kt.topk_fallback = 0;
   g.kt.topk_candidates = 0;
+  g.topk_pending = false;
   prof_record(0, s);
   if (p.direct) {
     RET(topk_direct(keys, rows, n, kk, out_rows, out_hi, s));
@@ -560,19 +592,86 @@ int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint6
     prof_record(3, s);
     CK(cudaStreamSynchronize(s));
   } else {
-    CK(cudaMemsetAsync(ctl(0), 0, sizeof(SelectCtl) * 2, s));
-    RET(launch_select(make_args(SrcSample{keys, rows, n, (uint32_t)std::max<uint64_t>(1, n / p.s)}, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), s));
+    // Small sample sets / candidate lists use the one-launch rank kernel; the
+    // radix engines (which need zeroed histograms) handle the rest.
+    const bool rank_thr = p.s <= kRankMax;
+    const bool rank_sel = p.expect <= kRankMax / 2 && kk <= kRankMax;
+    if (rank_thr && rank_sel && env_u64("GOLP_TOPK_FUSED", 1)) {
+      // everything in one cooperative launch, no host round trip (stream-ordered)
+      RET(ensure_status_words());
+      *reinterpret_cast<volatile int*>(g.status_host) = 0;
+      FusedTopkArgs f;
+      f.keys = keys;
+      f.rows = rows;
+      f.n = n;
+      f.need = kk;
+      f.s = (uint32_t)p.s;
+      f.need_s = (uint32_t)p.need_s;
+      f.w = (uint32_t)std::max<uint64_t>(1, n / p.s);
+      // test knobs: shrink the candidate buffer / rank limit to exercise the in-kernel fallbacks
+      f.cap = std::min<uint64_t>(p.cap, env_u64("GOLP_TOPK_CAP", p.cap));
+      f.rank_max = (uint32_t)std::min<uint64_t>(kRankMax, env_u64("GOLP_TOPK_RANK_MAX", kRankMax));
+      f.ctl = ctl(0);
+      f.cand_hi = g.cand_hi.as<uint64_t>();
+      f.cand_lo = g.cand_lo.as<uint32_t>();
+      f.w_hi = g.w_hi.as<uint64_t>();
+      f.w_lo = g.w_lo.as<uint32_t>();
+      f.out_rows = out_rows;
+      f.out_hi = out_hi;
+      f.host_count = reinterpret_cast<unsigned long long*>(g.status_dev + 8);
+      f.host_status = reinterpret_cast<int*>(g.status_dev);
+      static int blocks = 0;
+      const size_t smem = (size_t)kSortTile * (sizeof(uint64_t) + sizeof(uint32_t));
+      if (!blocks) {
+        CK(cudaFuncSetAttribute(topk_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, topk_fused_kernel, kSelThreads, smem));
+        if (per < 1) {
+          set_error("topk_fused_kernel cannot be co-resident");
+          return GOLP_ERR_CUDA;
+        }
+        blocks = per * g.sms;
+      }
+      void* args[] = {&f};
+      CK(cudaLaunchCooperativeKernel((void*)topk_fused_kernel, blocks, kSelThreads, args, smem, s));
+      ++g_launches;
+      prof_record(1, s);
+      prof_record(2, s);
+      prof_record(3, s);
+      g.topk_pending = true;  // candidate count / fallback resolved lazily
+      if (g.prof) {
+        g.kt.topk_threshold_ms = g.kt.topk_filter_ms = 0.0;
+        g.topk_timed = true;
+      }
+      return GOLP_OK;
+    }
+    if (!(rank_thr && rank_sel)) CK(cudaMemsetAsync(ctl(0), 0, sizeof(SelectCtl) * 2, s));
+    const SrcSample smp{keys, rows, n, (uint32_t)std::max<uint64_t>(1, n / p.s)};
+    if (rank_thr)
+      RET(launch_rank(make_args(smp, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), &ctl(1)->cand_count, s));
+    else
+      RET(launch_select(make_args(smp, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), s));
     prof_record(1, s);
     RET(launch_filter(keys, rows, n, p.cap, s));
     prof_record(2, s);
     RET(ensure_status_words());
-    RET(launch_select(cand_args(kk, p.cap, out_rows, out_hi), s));
+    if (rank_sel) RET(launch_rank(cand_args(kk, p.cap, out_rows, out_hi), nullptr, s));
+    else RET(launch_select(cand_args(kk, p.cap, out_rows, out_hi), s));
     prof_record(3, s);
-    int bad = 0;
+    int status = 0;
     uint64_t cands = 0;
-    RET(read_topk_status(s, &bad, &cands));
+    RET(read_topk_status(s, &status, &cands));
     g.kt.topk_candidates = cands;
-    if (bad) {
+    if (status == 2) {  // more candidates than the rank kernel holds: grid engine
+      char* c1 = reinterpret_cast<char*>(ctl(1));
+      CK(cudaMemsetAsync(c1, 0, offsetof(SelectCtl, cand_count), s));  // histograms
+      CK(cudaMemsetAsync(c1 + offsetof(SelectCtl, win_count), 0, sizeof(SelectCtl) - offsetof(SelectCtl, win_count),
+                         s));
+      RET(launch_select(cand_args(kk, p.cap, out_rows, out_hi), s));
+      prof_record(3, s);
+      RET(read_topk_status(s, &status, &cands));
+    }
+    if (status != 0) {
       g.kt.topk_fallback = 1;
       RET(topk_direct(keys, rows, n, kk, out_rows, out_hi, s));
       prof_record(3, s);
@@ -597,13 +696,6 @@ int grid_for(uint64_t n, int threads, int per_sm) {
 // Radix partitioning of the join (see join.cuh): slices of GOLP_JOIN_SLICE_BYTES
 // (default 16 MiB of slots) once the table exceeds two slices, at most
 // kMaxProbeParts slices.
-uint64_t env_u64(const char* name, uint64_t dflt) {
-  const char* v = getenv(name);
-  if (!v || !*v) return dflt;
-  char* end = nullptr;
-  const unsigned long long x = strtoull(v, &end, 0);
-  return (end && *end == 0) ? (uint64_t)x : dflt;
-}
 
 void plan_partitions(uint64_t cap) {
   const uint64_t slice_bytes = std::max<uint64_t>(64, env_u64("GOLP_JOIN_SLICE_BYTES", 16ull << 20));
@@ -954,6 +1046,16 @@ int golp_set_profiling(int on) {
 
 int golp_last_kernel_times(golp_kernel_times* out) {
   if (!out) return invalid("null output");
+  if (g.topk_pending) {
+    CK(cudaDeviceSynchronize());
+    g.kt.topk_candidates = *reinterpret_cast<volatile unsigned long long*>(g.status_host + 8);
+    g.kt.topk_fallback = *reinterpret_cast<volatile int*>(g.status_host) != 0;
+    g.topk_pending = false;
+  }
+  if (g.topk_timed) {
+    g.kt.topk_select_ms = prof_ms(0, 3);
+    g.topk_timed = false;
+  }
   if (g.build_timed) {
     CK(cudaEventSynchronize(g.ev[5]));
     g.kt.join_build_ms = prof_ms(4, 5);

@@ -195,8 +195,10 @@ __device__ void block_radix_select(const uint64_t* s_hi, const uint32_t* s_lo, u
   }
 }
 
+// The select engine as a device function so the fused Top-K kernel can run it
+// in place (same block size and dynamic shared memory as select_kernel).
 template <class Src>
-__global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs<Src> a) {
+__device__ void select_body(const SelectArgs<Src>& a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* s_hi = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* s_lo = reinterpret_cast<uint32_t*>(s_hi + kSortTile);
@@ -497,6 +499,97 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs<Src> a) 
   }
 }
 
+template <class Src>
+__global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs<Src> a) {
+  select_body(a);
+}
+
+// ---- rank selection (small lists, many blocks, no grid barrier) -------------------
+// For lists of at most kRankMax items every block stages the whole list in shared
+// memory and its warps compute exact ranks (items strictly better, ties broken by
+// index so ranks are a permutation) for a strided share of the items: O(n^2 / P)
+// compares spread over the GPU, one launch, no digit passes. THRESH mode writes the
+// item of rank need-1 as the threshold (and clears the candidate counter the filter
+// appends to); FULL mode writes every item of rank < need to out[rank].
+// Candidate lists (use_cand_count) larger than kRankMax but within the buffer set
+// status 2: the host then runs the grid engine over the same candidates.
+constexpr uint32_t kRankMax = 8192;
+constexpr int kRankThreads = 512;
+constexpr size_t kRankSmem = (size_t)kRankMax * (sizeof(uint64_t) + sizeof(uint32_t));
+
+// Exact ranks of the m items staged in shared memory, computed for a strided
+// share of the items by every warp of the grid (see above).
+__device__ __forceinline__ void rank_items(const uint64_t* s_hi, const uint32_t* s_lo, uint32_t m, uint64_t need,
+                                           int mode, SelectCtl* ctl, uint32_t* out_rows, uint64_t* out_hi) {
+  const unsigned lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += warps) {
+    const uint64_t hi = s_hi[i];
+    const uint32_t lo = s_lo[i];
+    uint32_t better = 0, eq = 0;
+    for (uint32_t j = lane; j < m; j += 32) {  // key codes only: the common case has no ties
+      const uint64_t h = s_hi[j];
+      better += h > hi;
+      eq += h == hi;
+    }
+    better = __reduce_add_sync(0xFFFFFFFFu, better);
+    if (__reduce_add_sync(0xFFFFFFFFu, eq) > 1) {  // equal keys: row, then index decides
+      uint32_t tb = 0;
+      for (uint32_t j = lane; j < m; j += 32) {
+        if (s_hi[j] != hi) continue;
+        const uint32_t l = s_lo[j];
+        tb += (l > lo) | ((l == lo) & (j < i));
+      }
+      better += __reduce_add_sync(0xFFFFFFFFu, tb);
+    }
+    if (lane == 0) {
+      if (mode == kModeThreshold) {
+        if (better == need - 1) {
+          ctl->thr_key = key_from_ord(hi);
+          ctl->thr_row = ~lo;
+          ctl->res_hi = hi;
+          ctl->res_lo = lo;
+          ctl->res_bits = 96;
+        }
+      } else if (better < need) {
+        out_rows[better] = ~lo;
+        if (out_hi) out_hi[better] = hi;
+      }
+    }
+  }
+}
+
+template <class Src>
+__global__ void __launch_bounds__(kRankThreads) rank_select_kernel(SelectArgs<Src> a,
+                                                                   unsigned long long* clear_count) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* s_hi = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* s_lo = reinterpret_cast<uint32_t*>(s_hi + kRankMax);
+  uint64_t n = a.n;
+  if (a.use_cand_count) {
+    const unsigned long long c = *(volatile unsigned long long*)&a.ctl->cand_count;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.host_count) *(volatile unsigned long long*)a.host_count = c;
+    if (c > a.cap || c < a.need || c > kRankMax) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const int st = (c > a.cap || c < a.need) ? 1 : 2;
+        a.ctl->status = st;
+        if (a.host_status) *(volatile int*)a.host_status = st;
+        __threadfence_system();
+      }
+      return;
+    }
+    n = c;
+  }
+  if (clear_count && blockIdx.x == 0 && threadIdx.x == 0) *clear_count = 0ull;
+  const uint32_t m = (uint32_t)n;
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    s_hi[i] = a.src.hi(i);
+    s_lo[i] = a.src.lo(i);
+  }
+  __syncthreads();
+  rank_items(s_hi, s_lo, m, a.need < n ? a.need : n, a.mode, a.ctl, a.out_rows, a.out_hi);
+}
+
 // ---- streaming filter ------------------------------------------------------------
 // Keeps every item with (key, row) >= (thr_key, thr_row) in Top-K order, i.e.
 // key > thr_key, or key == thr_key and row <= thr_row. Float compare gives the
@@ -511,12 +604,10 @@ __device__ __forceinline__ bool filter_keep(double k, double tk, uint32_t tr, co
   return false;
 }
 
-__global__ void __launch_bounds__(kFilterThreads) topk_filter_kernel(
-    const double* __restrict__ keys, const uint32_t* __restrict__ rows, uint64_t n, const SelectCtl* thr,
-    unsigned long long* cand_count, uint64_t* __restrict__ cand_hi, uint32_t* __restrict__ cand_lo,
-    uint64_t cap) {
-  const double tk = *(const volatile double*)&thr->thr_key;
-  const uint32_t tr = *(const volatile uint32_t*)&thr->thr_row;
+__device__ __forceinline__ void filter_body(const double* __restrict__ keys, const uint32_t* __restrict__ rows,
+                                            uint64_t n, double tk, uint32_t tr, unsigned long long* cand_count,
+                                            uint64_t* __restrict__ cand_hi, uint32_t* __restrict__ cand_lo,
+                                            uint64_t cap) {
   const uint64_t head = (((uintptr_t)keys & 15) != 0 && n > 0) ? 1 : 0;
   const uint64_t nv = (n - head) / 2;
   const uint64_t tail = head + 2 * nv;  // index of a leftover odd element (if < n)
@@ -572,6 +663,150 @@ __global__ void __launch_bounds__(kFilterThreads) topk_filter_kernel(
       }
     }
   }
+}
+
+
+__global__ void __launch_bounds__(kFilterThreads) topk_filter_kernel(
+    const double* __restrict__ keys, const uint32_t* __restrict__ rows, uint64_t n, const SelectCtl* thr,
+    unsigned long long* cand_count, uint64_t* __restrict__ cand_hi, uint32_t* __restrict__ cand_lo,
+    uint64_t cap) {
+  const double tk = *(const volatile double*)&thr->thr_key;
+  const uint32_t tr = *(const volatile uint32_t*)&thr->thr_row;
+  filter_body(keys, rows, n, tk, tr, cand_count, cand_hi, cand_lo, cap);
+}
+
+
+// ---- fused small Top-K -----------------------------------------------------------
+// One cooperative launch for inputs whose sample set and expected candidate list
+// fit the rank kernel (C1-sized): rank threshold over the samples | grid barrier |
+// streaming filter | grid barrier | rank select over the candidates. If the
+// candidate set turns out unusable it runs the grid select engine in place (over
+// the candidates when they fit the buffer but not shared memory, else straight
+// over the input), so the host never has to wait and decide.
+struct FusedTopkArgs {
+  const double* keys;
+  const uint32_t* rows;
+  uint64_t n;
+  uint64_t need;  // min(k, n)
+  uint32_t s;     // samples (<= kRankMax)
+  uint32_t need_s;
+  uint32_t w;     // sample stratum width
+  uint64_t cap;   // candidate buffer capacity
+  uint32_t rank_max;  // largest candidate list ranked in shared memory (<= kRankMax)
+  SelectCtl* ctl;  // ctl[0] threshold, ctl[1] candidates, ctl[2] direct fallback
+  uint64_t* cand_hi;
+  uint32_t* cand_lo;
+  uint64_t* w_hi;
+  uint32_t* w_lo;
+  uint32_t* out_rows;
+  uint64_t* out_hi;
+  unsigned long long* host_count;  // optional mapped word: candidate count
+  int* host_status;                // optional mapped word: 1 fell back to the direct select
+};
+
+__global__ void __launch_bounds__(kSelThreads) topk_fused_kernel(FusedTopkArgs f) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* s_hi = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* s_lo = reinterpret_cast<uint32_t*>(s_hi + kSortTile);
+  static_assert(kSortTile >= kRankMax, "rank lists are staged in the select tile");
+  cg::grid_group grid = cg::this_grid();
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+  {  // zero the candidate and fallback controls (histograms, counters, status)
+    unsigned* z = reinterpret_cast<unsigned*>(f.ctl + 1);
+    const uint64_t words = 2 * sizeof(SelectCtl) / sizeof(unsigned);
+    for (uint64_t i = gtid; i < words; i += gstride) z[i] = 0u;
+  }
+  const SrcSample smp{f.keys, f.rows, f.n, f.w};
+  constexpr int kGather = kRankMax / kSelThreads;  // all loads of a thread in flight together
+  {
+    uint64_t h[kGather];
+    uint32_t l[kGather];
+#pragma unroll
+    for (int u = 0; u < kGather; ++u) {
+      const uint32_t i = threadIdx.x + u * kSelThreads;
+      if (i < f.s) {
+        h[u] = smp.hi(i);
+        l[u] = smp.lo(i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGather; ++u) {
+      const uint32_t i = threadIdx.x + u * kSelThreads;
+      if (i < f.s) {
+        s_hi[i] = h[u];
+        s_lo[i] = l[u];
+      }
+    }
+  }
+  __syncthreads();
+  rank_items(s_hi, s_lo, f.s, f.need_s, kModeThreshold, f.ctl, nullptr, nullptr);
+  grid.sync();
+  const double tk = __ldcg(&f.ctl->thr_key);
+  const uint32_t tr = __ldcg(&f.ctl->thr_row);
+  filter_body(f.keys, f.rows, f.n, tk, tr, &f.ctl[1].cand_count, f.cand_hi, f.cand_lo, f.cap);
+  grid.sync();
+  const unsigned long long c = __ldcg(&f.ctl[1].cand_count);
+  if (gtid == 0 && f.host_count) *(volatile unsigned long long*)f.host_count = c;
+  if (c >= f.need && c <= f.cap) {
+    if (c <= f.rank_max) {
+      uint64_t h[kGather];
+      uint32_t l[kGather];
+#pragma unroll
+      for (int u = 0; u < kGather; ++u) {
+        const uint32_t i = threadIdx.x + u * kSelThreads;
+        if (i < c) {
+          h[u] = __ldcg(f.cand_hi + i);
+          l[u] = __ldcg(f.cand_lo + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kGather; ++u) {
+        const uint32_t i = threadIdx.x + u * kSelThreads;
+        if (i < c) {
+          s_hi[i] = h[u];
+          s_lo[i] = l[u];
+        }
+      }
+      __syncthreads();
+      rank_items(s_hi, s_lo, (uint32_t)c, f.need, kModeFull, nullptr, f.out_rows, f.out_hi);
+      return;
+    }
+    SelectArgs<SrcCand> a;
+    a.src = SrcCand{f.cand_hi, f.cand_lo};
+    a.n = c;
+    a.need = f.need;
+    a.cap = 0;
+    a.use_cand_count = 0;
+    a.mode = kModeFull;
+    a.ctl = f.ctl + 1;
+    a.w_hi = f.w_hi;
+    a.w_lo = f.w_lo;
+    a.out_rows = f.out_rows;
+    a.out_hi = f.out_hi;
+    a.host_status = nullptr;
+    a.host_count = nullptr;
+    __syncthreads();
+    select_body(a);
+    return;
+  }
+  if (gtid == 0 && f.host_status) *(volatile int*)f.host_status = 1;
+  SelectArgs<SrcInput> a;
+  a.src = SrcInput{f.keys, f.rows};
+  a.n = f.n;
+  a.need = f.need;
+  a.cap = 0;
+  a.use_cand_count = 0;
+  a.mode = kModeFull;
+  a.ctl = f.ctl + 2;
+  a.w_hi = f.w_hi;
+  a.w_lo = f.w_lo;
+  a.out_rows = f.out_rows;
+  a.out_hi = f.out_hi;
+  a.host_status = nullptr;
+  a.host_count = nullptr;
+  __syncthreads();
+  select_body(a);
 }
 
 }  // namespace golp

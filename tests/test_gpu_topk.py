@@ -81,6 +81,38 @@ def test_topk_duplicate_rows_force_exact_fallback(b200):
     assert got.tolist() == [7] * 50
 
 
+@pytest.mark.parametrize("env,fallback", [({}, 0), ({"GOLP_TOPK_CAP": "100"}, 1), ({"GOLP_TOPK_RANK_MAX": "64"}, 0),
+                                          ({"GOLP_TOPK_FUSED": "0"}, 0)])
+@pytest.mark.parametrize("kind", ["uniform", "small_domain", "zipf_hi"])
+def test_topk_fused_path_and_in_kernel_fallbacks(b200, monkeypatch, env, fallback, kind):
+    """C1-sized inputs run as one cooperative kernel; its in-kernel fallbacks
+    (candidate buffer overflow -> direct select over the input, candidate list
+    above the rank limit -> grid select over the candidates) must agree too."""
+    from paper_2601_19911_b200 import _native
+
+    for name, val in env.items():
+        monkeypatch.setenv(name, val)
+    rng = np.random.default_rng(77 + len(kind))
+    n, k = 1_000_000, 100
+    keys = _gen(kind, n, rng)
+    rows = rng.permutation(n).astype(np.uint32)
+    _native.check(_native.load().golp_set_profiling(1))
+    try:
+        got = b200.topk(KeyVector(keys, rows), k).payload.rows
+        kt = _native.kernel_times()
+    finally:
+        _native.check(_native.load().golp_set_profiling(0))
+    assert np.array_equal(got, oracle.topk(keys, rows, k))
+    assert kt["topk_fallback"] == fallback
+    assert kt["topk_candidates"] >= k
+
+
+def test_topk_fused_identical_items(b200):
+    n = 1_000_000  # identical (key, row) items: every item passes the threshold
+    got = b200.topk(KeyVector(np.full(n, -2.5), np.full(n, 11, dtype=np.uint32)), 30).payload.rows
+    assert got.tolist() == [11] * 30
+
+
 def test_topk_empty_and_bad_k(b200):
     res = b200.topk(KeyVector(np.empty(0), np.empty(0, dtype=np.uint32)), 100)
     assert len(res.payload.rows) == 0 and res.ledger.h2d_bytes == 0
