@@ -4,6 +4,7 @@
 // Boundary being replaced: the reference's device protocol topk()/probe()
 // (ProxyDevice, pkg/src/golp/device.py:299-436), whose ledgers feed the gate
 // (pkg/src/golp/gate.py:185-213) and calibrate_profile (device.py:490-554).
+#include <cerrno>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1162,17 +1163,22 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
   if (n <= per_chunk) {
     // One chunk: upload both columns, then the device-resident pipeline (the
     // samples are drawn on the device; nothing to overlap with).
+    const bool trace = std::getenv("GOLP_TRACE") != nullptr;
     RET(stage_h2d(dk, keys, n * 8));
+    if (trace) std::fprintf(stderr, "[golp] topk %.3f ms keys queued\n", (wall_seconds() - t0) * 1e3);
     RET(stage_h2d(dr, rows, n * 4));
     if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(n * (size_t)payload_bytes));
     CK(cudaEventRecord(ev_chunk, g.s_h2d));
+    if (trace) std::fprintf(stderr, "[golp] topk %.3f ms rows queued\n", (wall_seconds() - t0) * 1e3);
     CK(cudaEventSynchronize(ev_chunk));
     g.next_slot = 0;
     for (bool& b : g.pin_busy) b = false;
     const double t1 = wall_seconds();
+    if (trace) std::fprintf(stderr, "[golp] topk %.3f ms uploads done\n", (t1 - t0) * 1e3);
     CK(cudaStreamWaitEvent(s, ev_chunk, 0));
     uint32_t* d_out = g.out_rows.as<uint32_t>();
     RET(topk_device_impl(dk, dr, n, kk, d_out, nullptr, s));
+    CK(cudaStreamSynchronize(s));  // the fused path is stream-ordered: charge its time to t_kernel
     const double t2 = wall_seconds();
     uint32_t* hbuf = static_cast<uint32_t*>(g.pin_small);
     CK(cudaMemcpyAsync(hbuf, d_out, kk * 4, cudaMemcpyDeviceToHost, s));
@@ -1480,6 +1486,25 @@ int golp_host_is_pinned(const void* p) { return is_pinned(p) ? 1 : 0; }
 int golp_host_register(const void* p, uint64_t bytes) {
   RET(ensure_init());
   if (!p || !bytes) return invalid("empty range");
+  // DMA from registered memory runs at ~half the PCIe rate when the range is
+  // backed by 4 KB pages (measured: 12 MB in 0.45 ms vs 0.23 ms from huge
+  // pages). Ask the kernel to collapse the 2 MB-aligned interior into huge pages
+  // first (MADV_COLLAPSE, Linux >= 6.1; best effort, errors ignored).
+#ifndef MADV_COLLAPSE
+#define MADV_COLLAPSE 25
+#endif
+  {
+    constexpr uintptr_t kHuge = uintptr_t(2) << 20;
+    const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + kHuge - 1) & ~(kHuge - 1);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes) & ~(kHuge - 1);
+    if (e > a) {
+      madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
+      const int rc = madvise(reinterpret_cast<void*>(a), e - a, MADV_COLLAPSE);
+      if (std::getenv("GOLP_TRACE"))
+        std::fprintf(stderr, "[golp] register %p +%llu: collapse %llu bytes rc=%d errno=%d\n", p,
+                     (unsigned long long)bytes, (unsigned long long)(e - a), rc, rc ? errno : 0);
+    }
+  }
   CK(cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterReadOnly));
   return GOLP_OK;
 }

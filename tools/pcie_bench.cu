@@ -14,7 +14,7 @@
 static double now() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
 
 int main() {
-  const size_t sizes[] = {size_t(12) << 20, size_t(132) << 20, size_t(1) << 30};
+  const size_t sizes[] = {size_t(4) << 20, size_t(8) << 20, size_t(12) << 20, size_t(132) << 20};
   void* dev;
   cudaMalloc(&dev, size_t(1) << 30);
   printf("host threads: %u\n", std::thread::hardware_concurrency());
