@@ -65,6 +65,8 @@ typedef struct golp_kernel_times {
   uint64_t join_groups;     /* distinct build keys                         */
   uint64_t join_capacity;   /* hash-table slots                            */
   uint64_t join_slices;     /* table slices of a radix-partitioned join (1 = not partitioned) */
+  double full_sort_ms;      /* device time of the last full sort                     */
+  uint64_t full_sort_passes;/* digit passes it needed (of 12)                         */
 } golp_kernel_times;
 
 /* ---- lifecycle ---------------------------------------------------------------- */
@@ -103,6 +105,11 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
 /* Copy the M pairs of the last golp_probe into caller arrays of m = M entries
  * (the M > out_cap case). Adds t_d2h and d2h_bytes = 8*M to *led. */
 int golp_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m, golp_ledger* led);
+/* Full sort from host buffers (the fig3 full_sort baseline, harness.py:247-270,
+ * offloaded): out_rows gets all n row ids in host_full_sort order. Ledger as the
+ * device protocol: H2D = entry bytes * n, D2H = 4 * n. */
+int golp_full_sort(const double* keys, const uint32_t* rows, uint64_t n, int mode, uint32_t payload_bytes,
+                   uint32_t* out_rows, golp_ledger* led);
 /* Host memory for result arrays: a page-locked arena (so results are DMA'd
  * straight in), falling back to mmap + transparent huge pages. Owned by the
  * caller's result object, released with golp_host_free(ptr, bytes). */
@@ -141,6 +148,13 @@ int golp_join_probe_device(const double* d_probe_keys, const uint32_t* d_probe_r
 int golp_join_probe_device_async(const double* d_probe_keys, const uint32_t* d_probe_rows, uint64_t np,
                                  uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
                                  uint64_t* d_out_matches, void* stream);
+
+/* Full sort on the device: host_full_sort (host.py:127-130, np.lexsort((rows,
+ * keys))) -- d_out_rows gets the n row ids ordered by key ascending (-0.0 ==
+ * +0.0), equal keys by ascending row id. Stream-ordered (synchronizes once
+ * after its histogram pass to plan the digit passes). */
+int golp_full_sort_device(const double* d_keys, const uint32_t* d_rows, uint64_t n, uint32_t* d_out_rows,
+                          void* stream);
 
 /* ---- classical host engine (the gate's HOST path, gate.py:193-194,209-210) ------ */
 /* Multi-threaded CPU Top-K with host_topk's exact output (host.py:133-144). */

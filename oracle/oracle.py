@@ -76,6 +76,13 @@ def topk(keys, rows, k: int) -> np.ndarray:
     return out
 
 
+def full_sort(keys, rows) -> np.ndarray:
+    """host_full_sort rows (host.py:127-130): np.lexsort((rows, keys)) order --
+    key ascending (float compare, so -0.0 ties +0.0), then row id ascending."""
+    kc, rc = _cols(keys, rows)
+    return rc[np.lexsort((rc, kc))]
+
+
 def proxy_topk(keys, rows, k: int, workers: int) -> np.ndarray:
     """ProxyDevice.topk answer with `workers` threads (device.py:329-380)."""
     kc, rc = _cols(keys, rows)

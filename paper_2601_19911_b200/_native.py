@@ -55,6 +55,8 @@ class KernelTimes(C.Structure):
         ("join_groups", C.c_uint64),
         ("join_capacity", C.c_uint64),
         ("join_slices", C.c_uint64),
+        ("full_sort_ms", C.c_double),
+        ("full_sort_passes", C.c_uint64),
     ]
 
 
@@ -76,6 +78,8 @@ SIGNATURES = {
     "golp_join_build_device": (_int, [_vp, _vp, _u64, _vp]),
     "golp_join_probe_device": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, C.POINTER(_u64), _vp]),
     "golp_join_probe_device_async": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
+    "golp_full_sort": (_int, [_vp, _vp, _u64, _int, _u32, _vp, C.POINTER(Ledger)]),
+    "golp_full_sort_device": (_int, [_vp, _vp, _u64, _vp, _vp]),
     "golp_host_alloc": (_vp, [_u64]),
     "golp_host_free": (_int, [_vp, _u64]),
     "golp_host_register": (_int, [_vp, _u64]),

@@ -16,6 +16,7 @@
 #include "../../include/golp_b200.h"
 #include "join.cuh"
 #include "runtime.h"
+#include "sort.cuh"
 #include "topk.cuh"
 
 namespace golp {
@@ -112,6 +113,7 @@ struct Ctx {
   DevBuf sc_prow, sc_off, sc_cnt;
   DevBuf part_keys, part_pos, part_cnt, part_cur, run_base, run_len, res_part, work_ctr;
   DevBuf pairs_p, pairs_b;
+  DevBuf srt_hist, srt_k0, srt_k1, srt_r0, srt_r1, srt_status, srt_base;
   DevBuf in_keys, in_rows, in_bkeys, in_brows, in_payload;
   uint64_t jcap = 0, jmask = 0, jnb = 0;
   uint32_t jparts = 1;  // table slices of the radix-partitioned join (1 = not partitioned)
@@ -974,6 +976,96 @@ int check_mode(int mode, uint32_t payload_bytes, uint64_t* entry) {
   return invalid("unknown transfer mode");
 }
 
+
+// ---- full sort ----------------------------------------------------------------------
+// host_full_sort on the device (sort.cuh): histogram pass, host picks the digits
+// that need a pass (row digits only when the rows are not ascending; no
+// single-bucket digits), then one onesweep pass per digit. The last pass writes
+// only the rows, straight into out_rows.
+int full_sort_impl(const double* keys, const uint32_t* rows, uint64_t n, uint32_t* out_rows, cudaStream_t s) {
+  g.kt.full_sort_passes = 0;
+  if (n == 0) return GOLP_OK;
+  prof_record(0, s);
+  CK(g.srt_hist.ensure(kSortDigits * 256 * 8 + 8));
+  unsigned long long* hist = g.srt_hist.as<unsigned long long>();
+  unsigned* unsorted = reinterpret_cast<unsigned*>(hist + kSortDigits * 256);
+  CK(cudaMemsetAsync(hist, 0, kSortDigits * 256 * 8 + 8, s));
+  sort_hist_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(keys, rows, n, hist, unsorted);
+  CKL();
+  ++g_launches;
+  unsigned long long* hh = static_cast<unsigned long long*>(g.pin_small);
+  CK(cudaMemcpyAsync(hh, hist, kSortDigits * 256 * 8 + 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const bool rows_sorted = *reinterpret_cast<const unsigned*>(hh + kSortDigits * 256) == 0;
+  int digits[kSortDigits];
+  int nd = 0;
+  for (int d = 0; d < kSortDigits; ++d) {
+    if (d < 4 && rows_sorted) continue;
+    bool trivial = false;
+    for (int b = 0; b < 256; ++b) trivial |= hh[d * 256 + b] == n;
+    if (!trivial) digits[nd++] = d;
+  }
+  g.kt.full_sort_passes = (uint64_t)nd;
+  if (nd == 0) {  // every item has the same code and the rows are in order already
+    CK(cudaMemcpyAsync(out_rows, rows, n * 4, cudaMemcpyDeviceToDevice, s));
+    prof_record(1, s);
+    return GOLP_OK;
+  }
+  // exclusive global offsets of every digit that gets a pass
+  unsigned long long* base = hh + kSortDigits * 256 + 8;
+  for (int i = 0; i < nd; ++i) {
+    unsigned long long run = 0;
+    for (int b = 0; b < 256; ++b) {
+      base[i * 256 + b] = run;
+      run += hh[digits[i] * 256 + b];
+    }
+  }
+  CK(g.srt_base.ensure((size_t)nd * 256 * 8));
+  CK(cudaMemcpyAsync(g.srt_base.p, base, (size_t)nd * 256 * 8, cudaMemcpyHostToDevice, s));
+  const uint64_t ntiles = (n + kSortTileN - 1) / kSortTileN;
+  CK(g.srt_status.ensure(ntiles * 256 * 8 + 8));
+  if (nd > 1) {
+    CK(g.srt_k0.ensure(n * 8));
+    CK(g.srt_r0.ensure(n * 4));
+  }
+  if (nd > 2) {
+    CK(g.srt_k1.ensure(n * 8));
+    CK(g.srt_r1.ensure(n * 4));
+  }
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(sort_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem));
+    attr = true;
+  }
+  unsigned long long* status = g.srt_status.as<unsigned long long>();
+  unsigned long long* ctr = status + ntiles * 256;
+  const uint64_t* in_k = nullptr;
+  const uint32_t* in_r = rows;
+  for (int i = 0; i < nd; ++i) {
+    const bool last = i + 1 == nd;
+    uint64_t* ok = last ? nullptr : (i % 2 == 0 ? g.srt_k0.as<uint64_t>() : g.srt_k1.as<uint64_t>());
+    uint32_t* orow = last ? out_rows : (i % 2 == 0 ? g.srt_r0.as<uint32_t>() : g.srt_r1.as<uint32_t>());
+    CK(cudaMemsetAsync(status, 0, ntiles * 256 * 8 + 8, s));
+    SortPassArgs a;
+    a.in_f64 = i == 0 ? keys : nullptr;
+    a.in_keys = in_k;
+    a.in_rows = in_r;
+    a.out_keys = ok;
+    a.out_rows = orow;
+    a.n = n;
+    a.digit = digits[i];
+    a.digit_base = g.srt_base.as<unsigned long long>() + (size_t)i * 256;
+    a.status = status;
+    a.tile_ctr = ctr;
+    sort_pass_kernel<<<(unsigned)ntiles, kSortThreads, kSortSmem, s>>>(a);
+    CKL();
+    ++g_launches;
+    in_k = ok;
+    in_r = orow;
+  }
+  prof_record(1, s);
+  return GOLP_OK;
+}
 }  // namespace
 
 // =====================================================================================
@@ -992,7 +1084,7 @@ int golp_shutdown(void) {
   g.pool.stop();
   DevBuf* bufs[] = {&g.ctl, &g.cand_hi, &g.cand_lo, &g.w_hi, &g.w_lo, &g.out_rows, &g.out_hi, &g.samples,
                     &g.table, &g.rows_arr, &g.ovf, &g.big_list, &g.jcount,
-                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.in_keys, &g.in_rows,
+                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.srt_hist, &g.srt_k0, &g.srt_k1, &g.srt_r0, &g.srt_r1, &g.srt_status, &g.srt_base, &g.in_keys, &g.in_rows,
                     &g.in_bkeys, &g.in_brows, &g.in_payload};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < kSlots; ++i) {
@@ -1078,6 +1170,59 @@ int golp_topk_device(const double* d_keys, const uint32_t* d_rows, uint64_t n, u
   RET(ensure_init());
   if (n > 0 && (!d_keys || !d_rows || !d_out_rows)) return invalid("null device pointer");
   return topk_device_impl(d_keys, d_rows, n, k, d_out_rows, d_out_keys, as_stream(stream));
+}
+
+int golp_full_sort_device(const double* d_keys, const uint32_t* d_rows, uint64_t n, uint32_t* d_out_rows,
+                          void* stream) {
+  RET(ensure_init());
+  if (n > 0 && (!d_keys || !d_rows || !d_out_rows)) return invalid("null device pointer");
+  cudaStream_t s = as_stream(stream);
+  RET(full_sort_impl(d_keys, d_rows, n, d_out_rows, s));
+  if (g.prof) {
+    CK(cudaStreamSynchronize(s));
+    g.kt.full_sort_ms = prof_ms(0, 1);
+  }
+  return GOLP_OK;
+}
+
+int golp_full_sort(const double* keys, const uint32_t* rows, uint64_t n, int mode, uint32_t payload_bytes,
+                   uint32_t* out_rows, golp_ledger* led) {
+  uint64_t entry = 0;
+  RET(check_mode(mode, payload_bytes, &entry));
+  if (!led) return invalid("null ledger");
+  RET(ensure_init());
+  const double t0 = wall_seconds();
+  *led = golp_ledger{entry * n, 4 * n, 0.0, 0.0, 0.0, 0.0};
+  if (n == 0) return GOLP_OK;
+  if (!keys || !rows || !out_rows) return invalid("null buffer");
+  cudaStream_t s = g.s_main;
+  CK(g.in_keys.ensure(n * 8));
+  CK(g.in_rows.ensure(n * 4));
+  CK(g.out_rows.ensure(n * 4));
+  RET(stage_h2d(g.in_keys.p, keys, n * 8));
+  RET(stage_h2d(g.in_rows.p, rows, n * 4));
+  if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(n * (size_t)payload_bytes));
+  cudaEvent_t ev_up = g.ev[2];
+  CK(cudaEventRecord(ev_up, g.s_h2d));
+  CK(cudaEventSynchronize(ev_up));
+  g.next_slot = 0;
+  for (bool& b : g.pin_busy) b = false;
+  const double t1 = wall_seconds();
+  CK(cudaStreamWaitEvent(s, ev_up, 0));
+  RET(full_sort_impl(g.in_keys.as<double>(), g.in_rows.as<uint32_t>(), n, g.out_rows.as<uint32_t>(), s));
+  CK(cudaStreamSynchronize(s));
+  if (g.prof) g.kt.full_sort_ms = prof_ms(0, 1);
+  const double t2 = wall_seconds();
+  if (is_pinned(out_rows)) {
+    CK(cudaMemcpyAsync(out_rows, g.out_rows.p, n * 4, cudaMemcpyDeviceToHost, g.s_d2h));
+    CK(cudaStreamSynchronize(g.s_d2h));
+  } else {
+    RET(stage_d2h(out_rows, g.out_rows.p, n * 4));
+  }
+  led->t_h2d = t1 - t0;
+  led->t_kernel = t2 - t1;
+  led->t_d2h = wall_seconds() - t2;
+  return GOLP_OK;
 }
 
 int golp_topk_merge_device(const uint64_t* d_key_codes, const uint32_t* d_rows, uint64_t n, uint64_t k,

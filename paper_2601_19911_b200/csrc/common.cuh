@@ -100,6 +100,36 @@ __device__ __forceinline__ unsigned long long warp_append(unsigned long long* co
   return base + __popc(mask & ((1u << lane) - 1u));
 }
 
+// Block-wide exclusive scan (blockDim <= 1024; every thread must call it).
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* s_w,
+                                                              unsigned long long* total) {
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  unsigned long long incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if ((int)lane >= o) incl += u;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long w = lane < (blockDim.x >> 5) ? s_w[lane] : 0ull;
+    unsigned long long wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if ((int)lane >= o) wi += u;
+    }
+    if (lane < (blockDim.x >> 5)) s_w[lane] = wi - w;
+    if (lane == 31) s_w[32] = wi;
+  }
+  __syncthreads();
+  const unsigned long long r = s_w[warp] + incl - v;
+  *total = s_w[32];
+  __syncthreads();
+  return r;
+}
+
 __device__ __forceinline__ double2 ldg_nc_d2(const double* p) {
   double2 r;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));

@@ -401,35 +401,6 @@ __device__ __forceinline__ uint4 ldg_stream_u4(const uint32_t* p, uint64_t pol) 
 // ---- block scan helpers ----------------------------------------------------------
 constexpr int kScanThreads = 1024;
 
-__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* s_w,
-                                                              unsigned long long* total) {
-  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  unsigned long long incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if ((int)lane >= o) incl += u;
-  }
-  if (lane == 31) s_w[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const unsigned long long w = lane < (blockDim.x >> 5) ? s_w[lane] : 0ull;
-    unsigned long long wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, wi, o);
-      if ((int)lane >= o) wi += u;
-    }
-    if (lane < (blockDim.x >> 5)) s_w[lane] = wi - w;
-    if (lane == 31) s_w[32] = wi;
-  }
-  __syncthreads();
-  const unsigned long long r = s_w[warp] + incl - v;
-  *total = s_w[32];
-  __syncthreads();
-  return r;
-}
-
 // One block: exclusive scan of the partials, offset by *base_in; writes *total_out.
 __global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(unsigned long long* partial, uint32_t nparts,
                                                                      const unsigned long long* base_in,

@@ -110,5 +110,15 @@ def join(bkeys, brows, pkeys, prows, capacity: int | None = None, stream=None):
         return op[: m.value], ob[: m.value]
 
 
+def full_sort(keys: torch.Tensor, rows: torch.Tensor, stream=None) -> torch.Tensor:
+    """Row ids (int32 storage of u32) by key ascending, equal keys by ascending
+    row id -- host_full_sort (pkg/src/golp/host.py:127-130) on the device."""
+    _check_cols(keys, rows)
+    out = torch.empty(keys.numel(), dtype=torch.int32, device=keys.device)
+    _native.check(_native.load().golp_full_sort_device(keys.data_ptr(), rows.data_ptr(), keys.numel(),
+                                                       out.data_ptr() if keys.numel() else 0, _stream(stream)))
+    return out
+
+
 def set_profiling(on: bool) -> None:
     _native.check(_native.load().golp_set_profiling(1 if on else 0))

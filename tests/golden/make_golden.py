@@ -199,15 +199,54 @@ def gate_cases(golp, device, gate, harness):
     (OUT / "gate.json").write_text(json.dumps(out, indent=0))
 
 
-def main():
+def full_sort_cases(golp, host, store):
+    """host_full_sort (pkg/src/golp/host.py:127-130) known answers."""
+    pk = Packer()
+
+    def add(keys, rows, tag):
+        kv = store.KeyVector(keys=np.asarray(keys, dtype=np.float64), rows=np.asarray(rows, dtype=np.uint32))
+        pk.add({"keys": kv.keys, "rows": kv.rows, "expect": host.host_full_sort(kv)}, tag=tag)
+
+    add([5, 1, 9, 3], range(4), "hand")
+    add([7, 7, 7, 7], [9, 2, 5, 1], "ties")
+    add([0.0, -0.0, 0.0, -1.0], [5, 2, 9, 1], "neg_zero")
+    big = np.array([2**53, 2**53 + 1, 2**53 - 1], dtype=np.int64).astype(np.float64)
+    add(big, [7, 3, 0], "beyond_2p53")
+    add([-3.5, -1e300, 1e300, -0.0, 0.0, 5e-324, -5e-324], [6, 5, 4, 3, 2, 1, 0], "extremes")
+    add([1.0], [0], "single")
+    rng = np.random.default_rng(127)
+    for i in range(30):
+        n = int(10 ** rng.uniform(1, 4.3))
+        if i % 3 == 0:
+            keys = rng.integers(-4, 5, size=n).astype(np.float64)
+            keys[rng.random(n) < 0.2] = -0.0
+        elif i % 3 == 1:
+            keys = rng.standard_normal(n)
+        else:
+            keys = rng.integers(0, 2**53, size=n, dtype=np.int64).astype(np.float64)
+        rows = np.arange(n) if i % 2 else rng.permutation(n)
+        add(keys, rows, "random")
+    pk.save(OUT / "full_sort.npz")
+
+
+GENERATORS = ("topk", "probe", "table", "gate", "full_sort")
+
+
+def main(which=GENERATORS):
     golp, device, gate, harness, host, store = _ref()
-    topk_cases(golp, host, store)
-    probe_cases(golp, host, store)
-    table_layout(golp, host, store)
-    gate_cases(golp, device, gate, harness)
+    if "topk" in which:
+        topk_cases(golp, host, store)
+    if "probe" in which:
+        probe_cases(golp, host, store)
+    if "table" in which:
+        table_layout(golp, host, store)
+    if "gate" in which:
+        gate_cases(golp, device, gate, harness)
+    if "full_sort" in which:
+        full_sort_cases(golp, host, store)
     for p in sorted(OUT.glob("*.npz")) + [OUT / "gate.json"]:
         print(p.name, p.stat().st_size)
 
 
 if __name__ == "__main__":
-    main()
+    main(tuple(sys.argv[1:]) or GENERATORS)

@@ -54,3 +54,8 @@ def test_oracle_proxy_ports_agree_with_oracle(workers):
     p1, b1 = t.probe(keys, rows, workers=1)
     pw, bw = t.probe(keys, rows, workers=workers)
     assert np.array_equal(p1, pw) and np.array_equal(b1, bw)
+
+
+@pytest.mark.parametrize("case", cases("full_sort"), ids=lambda c: f"{c['tag']}-n{len(c['keys'])}")
+def test_oracle_full_sort_matches_reference(case):
+    assert oracle.full_sort(case["keys"], case["rows"]).tolist() == case["expect"].tolist()
