@@ -12,6 +12,7 @@ with golp (out of scope).
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass
 from typing import NamedTuple, Optional, Sequence
 
@@ -19,8 +20,8 @@ import numpy as np
 
 from .device import DEFAULT_MODELED_PROFILE, FULL_ROW, KEY_ONLY, OP_PROBE, OP_TOPK, ModeledDevice, calibrate_profile
 from .errors import StrategyMismatchError
-from .gate import DEVICE, HOST, GateConfig, execute_gated, execute_path
-from .host import mix64
+from .gate import DEFAULT_CPU_MODEL, DEVICE, HOST, OP_FULL_SORT, GateConfig, estimate_cpu_cost, execute_gated, execute_path
+from .host import host_full_sort, host_topk, mix64
 from .store import DEFAULT_PAYLOAD_BYTES, ColumnTable, generate_table, random_key_vector
 
 HOST_ONLY = "host_only"
@@ -109,6 +110,57 @@ class StrategyRun:
 
 def table_seed(spec_seed: int, n: int) -> int:
     return (spec_seed ^ mix64(n)) & _M64
+
+
+class ScalingRow(NamedTuple):
+    """One fig3 cell (harness.py:160-164)."""
+
+    n: int
+    op: str
+    median_s: float
+    p95_s: float
+
+
+def run_scaling_baseline(spec: WorkloadSpec, backend: str = "modeled", cpu_model=None, device=None) -> list:
+    """Cost per n of full_sort and topk -- the fig3 rows (harness.py:242-280).
+
+    "modeled" reports the CPU cost model; any other backend wall-clock times the
+    host primitives (one warmup run per cell). With `device` (a B200Device) the
+    same cells are timed through the offload path as well, ops suffixed
+    "@b200" (E2E wall time of device.full_sort / device.topk from host arrays),
+    and each device answer is checked against the host primitive.
+    """
+    model = cpu_model if cpu_model is not None else DEFAULT_CPU_MODEL
+    rows: list = []
+    if backend == "modeled":
+        for n in spec.n_grid:
+            for op in (OP_FULL_SORT, OP_TOPK):
+                v = estimate_cpu_cost(model, op, n, spec.k)
+                rows.append(ScalingRow(n, op, v, v))
+        return rows
+    wall = lambda: time.perf_counter_ns() / 1e9  # noqa: E731
+    for n in spec.n_grid:
+        kv = random_key_vector(n, table_seed(spec.seed, n))
+        cells = [(OP_FULL_SORT, lambda: host_full_sort(kv)), (OP_TOPK, lambda: host_topk(kv, spec.k))]
+        if device is not None:
+            sort_ref = host_full_sort(kv)
+            topk_ref = host_topk(kv, spec.k).rows
+            if not np.array_equal(device.full_sort(kv).payload, sort_ref):
+                raise StrategyMismatchError(f"device full_sort differs from host_full_sort at n={n}")
+            if not np.array_equal(device.topk(kv, spec.k).payload.rows, topk_ref):
+                raise StrategyMismatchError(f"device topk differs from host_topk at n={n}")
+            cells += [(OP_FULL_SORT + "@b200", lambda: device.full_sort(kv)),
+                      (OP_TOPK + "@b200", lambda: device.topk(kv, spec.k))]
+        for op, run in cells:
+            run()
+            samples = []
+            for _ in range(spec.repeats):
+                t0 = wall()
+                run()
+                samples.append(wall() - t0)
+            st = compute_stats(samples)
+            rows.append(ScalingRow(n, op, st.median, st.p95))
+    return rows
 
 
 def query_sizes(spec: WorkloadSpec) -> list:

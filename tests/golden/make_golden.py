@@ -196,6 +196,8 @@ def gate_cases(golp, device, gate, harness):
     for seq in ([1.0], [3.0, 1.0, 2.0], list(np.linspace(0, 1, 101)), [5, 5, 1, 9, 2, 2, 7]):
         s = harness.compute_stats(seq)
         out["stats"].append([list(map(float, seq)), s.median, s.p95, s.p99, s.mean])
+    spec = harness.WorkloadSpec(n_grid=(1_000, 100_000, 10**9), k=100, repeats=3)
+    out["scaling_modeled"] = [list(r) for r in harness.run_scaling_baseline(spec, backend="modeled")]
     (OUT / "gate.json").write_text(json.dumps(out, indent=0))
 
 

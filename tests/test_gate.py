@@ -177,3 +177,19 @@ def test_materialize_join_gathers_both_sides_in_pair_order():
     bad = type(res)(np.array([0], np.uint32), np.array([10**6], np.uint32), 1)
     with pytest.raises(IndexError):
         materialize_join(b, p, bad)
+
+
+def test_scaling_baseline_modeled_matches_reference():
+    from paper_2601_19911_b200.harness import WorkloadSpec, run_scaling_baseline
+
+    spec = WorkloadSpec(n_grid=(1_000, 100_000, 10**9), k=100, repeats=3)
+    got = [list(r) for r in run_scaling_baseline(spec, backend="modeled")]
+    assert got == gate_golden()["scaling_modeled"]
+
+
+def test_scaling_baseline_host_wall_clock_rows():
+    from paper_2601_19911_b200.harness import WorkloadSpec, run_scaling_baseline
+
+    rows = run_scaling_baseline(WorkloadSpec(n_grid=(100, 2_000), k=10, repeats=2), backend="host")
+    assert [(r.n, r.op) for r in rows] == [(100, "full_sort"), (100, "topk"), (2_000, "full_sort"), (2_000, "topk")]
+    assert all(0 < r.median_s <= r.p95_s for r in rows)

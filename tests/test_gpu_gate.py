@@ -45,3 +45,13 @@ def test_execute_gated_offloads_large_queries(b200):
     t = generate_table(3_000_000, 4, seed=2)
     res, d, lat = execute_gated(t, OP_TOPK, 100, GateConfig(), device=b200)
     assert d.path == DEVICE and len(res) == 100 and lat > 0
+
+
+def test_scaling_baseline_with_b200_rows(b200):
+    from paper_2601_19911_b200.harness import WorkloadSpec, run_scaling_baseline
+
+    rows = run_scaling_baseline(WorkloadSpec(n_grid=(10_000, 200_000), k=100, repeats=3), backend="host",
+                                device=b200)
+    ops = {(r.n, r.op) for r in rows}
+    assert (200_000, "full_sort@b200") in ops and (200_000, "topk@b200") in ops
+    assert all(r.median_s > 0 for r in rows)
