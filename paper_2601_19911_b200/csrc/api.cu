@@ -885,11 +885,13 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
   unsigned long long* tmp = g.totals2.as<unsigned long long>();
   // Partition the probe side (in spans of kSpan probes) when a span reuses each
   // table slice several times: span * 32 B of slot-pair reads >= 2x the table.
-  constexpr uint64_t kSpan = 1ull << 30;
+  // (GOLP_JOIN_SPAN shrinks the span so tests cover several spans on small inputs.)
+  const uint64_t kSpan = std::max<uint64_t>(kPartTile, env_u64("GOLP_JOIN_SPAN", 1ull << 30) / kPartTile * kPartTile);
   const uint64_t force = env_u64("GOLP_JOIN_PART_PROBE", 2);
   const bool part_probe =
       g.jparts > 1 && (force == 1 || (force == 2 && std::min(np, kSpan) >= g.jcap));
   const uint64_t span = part_probe ? kSpan : np;
+  uint64_t ci = 0;  // running sub-chunk index (pair-offset chaining)
   for (uint64_t s0 = 0; s0 < np; s0 += span) {
     const uint64_t sn = std::min(span, np - s0);
     if (part_probe) RET(probe_partitioned(pkeys + s0, sn, s));
@@ -922,10 +924,10 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
                                                                      g.jmask, sc, nwt, per_warp, part);
       }
       CKL();
-      const uint64_t ci = c0 / kSub;  // kSpan is a multiple of kSub
       const bool last = c0 + cn >= np;
-      const unsigned long long* bin = c0 == 0 ? base_in : tmp + (ci & 1);
+      const unsigned long long* bin = ci == 0 ? base_in : tmp + (ci & 1);
       unsigned long long* bout = last ? total_out : tmp + ((ci + 1) & 1);
+      ++ci;
       scan_partials_kernel<<<1, kScanThreads, 0, s>>>(part, (uint32_t)blocks, bin, bout);
       CKL();
       join_emit_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(sc, g.rows_arr.as<uint32_t>(), nwt, per_warp,

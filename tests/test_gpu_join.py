@@ -152,3 +152,48 @@ def test_partitioned_join_resident_subchunks(cuda, monkeypatch):
     ep, eb = oracle.join(bk, br, pk, pr)
     assert np.array_equal(op.cpu().numpy().view(np.uint32), ep)
     assert np.array_equal(ob.cpu().numpy().view(np.uint32), eb)
+
+
+@pytest.mark.parametrize("span", ["4096", "12288"])
+def test_partitioned_join_multi_span(b200, monkeypatch, span):
+    """Probe sides longer than a span are partitioned span by span; pair offsets
+    chain across spans and sub-chunks."""
+    monkeypatch.setenv("GOLP_JOIN_SLICE_BYTES", "4096")
+    monkeypatch.setenv("GOLP_JOIN_PART_PROBE", "1")
+    monkeypatch.setenv("GOLP_JOIN_SPAN", span)
+    rng = np.random.default_rng(int(span))
+    nb, np_ = 40_000, 90_001
+    bk = rng.integers(0, 60_000, size=nb).astype(np.float64)
+    pk = rng.integers(0, 60_000, size=np_).astype(np.float64)
+    br = rng.permutation(nb).astype(np.uint32)
+    pr = rng.permutation(np_).astype(np.uint32)
+    res = b200.probe(KeyVector(bk, br), KeyVector(pk, pr))
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert np.array_equal(res.payload.probe_rows, ep)
+    assert np.array_equal(res.payload.build_rows, eb)
+
+
+def test_partitioned_join_natural_scale(cuda):
+    """A table above the partitioning threshold with default settings (1 GiB
+    table, 64 slices, probe side partitioned) against the oracle."""
+    import torch
+
+    from paper_2601_19911_b200 import _native, resident
+
+    rng = np.random.default_rng(21)
+    nb, np_ = 20_000_000, 60_000_000
+    bk = rng.integers(0, 2 * nb, size=nb).astype(np.float64)
+    pk = rng.integers(0, 2 * nb, size=np_).astype(np.float64)
+    br = rng.permutation(nb).astype(np.uint32)
+    pr = np.arange(np_, dtype=np.uint32)
+    t = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(cuda)  # noqa: E731
+    resident.set_profiling(True)
+    try:
+        op, ob = resident.join(t(bk), t(br), t(pk), t(pr))
+        kt = _native.kernel_times()
+    finally:
+        resident.set_profiling(False)
+    assert kt["join_slices"] > 1
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert np.array_equal(op.cpu().numpy().view(np.uint32), ep)
+    assert np.array_equal(ob.cpu().numpy().view(np.uint32), eb)
