@@ -531,7 +531,14 @@ int launch_filter(const double* keys, const uint32_t* rows, uint64_t n, uint64_t
 }
 
 void prof_record(int idx, cudaStream_t s) {
-  if (g.prof) cudaEventRecord(g.ev[idx], s);
+  if (!g.prof) return;
+  // Inside a CUDA-graph capture the record must be an external event node, or
+  // the event cannot be synchronized / timed after a replay.
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(g.ev[idx], s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(g.ev[idx], s);
 }
 double prof_ms(int a, int b) {
   float ms = 0.f;
@@ -587,6 +594,7 @@ int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint6
   g.kt.topk_fallback = 0;
   g.kt.topk_candidates = 0;
   g.topk_pending = false;
+  g.topk_timed = false;
   prof_record(0, s);
   if (p.direct) {
     RET(topk_direct(keys, rows, n, kk, out_rows, out_hi, s));
@@ -1136,30 +1144,30 @@ uint64_t golp_launch_count(void) { return g_launches.load(); }
 int golp_set_profiling(int on) {
   RET(ensure_init());
   g.prof = on != 0;
+  g.build_timed = g.probe_timed = g.topk_timed = false;
   return GOLP_OK;
 }
 
+// The timing flags stay set while profiling is on, so a CUDA graph that captured
+// the event records can be replayed and read again after every replay.
 int golp_last_kernel_times(golp_kernel_times* out) {
   if (!out) return invalid("null output");
   if (g.topk_pending) {
     CK(cudaDeviceSynchronize());
     g.kt.topk_candidates = *reinterpret_cast<volatile unsigned long long*>(g.status_host + 8);
     g.kt.topk_fallback = *reinterpret_cast<volatile int*>(g.status_host) != 0;
-    g.topk_pending = false;
   }
   if (g.topk_timed) {
+    CK(cudaEventSynchronize(g.ev[3]));
     g.kt.topk_select_ms = prof_ms(0, 3);
-    g.topk_timed = false;
   }
   if (g.build_timed) {
     CK(cudaEventSynchronize(g.ev[5]));
     g.kt.join_build_ms = prof_ms(4, 5);
-    g.build_timed = false;
   }
   if (g.probe_timed) {
     CK(cudaEventSynchronize(g.ev[7]));
     g.kt.join_probe_ms = prof_ms(6, 7);
-    g.probe_timed = false;
   }
   *out = g.kt;
   return GOLP_OK;
