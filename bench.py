@@ -69,10 +69,21 @@ def join_data(wl: dict, rank: int):
 
 
 def topk_data(wl: dict, rank: int):
+    """Uniform keys (random_keys, store.py:165-171) or the SURVEY 8(d) Zipf variants:
+    r = PCG64(11).zipf(1.2, N) clipped to 2^53-1; "zipf_hi" key = (2^53-1) - r (the
+    most frequent rank is the largest key: K reduces to the smallest row ids among
+    the ties), "zipf_lo" key = r (the heavy tail sets the threshold)."""
     seed = wl["seed"] if rank == 0 else [wl["seed"], rank]
-    rng = np.random.Generator(np.random.PCG64(seed))
     n = wl["n"]
-    return rng.integers(0, 2**53, size=n, dtype=np.int64).astype(np.float64), np.arange(n, dtype=np.uint32)
+    dist = wl.get("dist", "uniform")
+    if dist == "uniform":
+        rng = np.random.Generator(np.random.PCG64(seed))
+        keys = rng.integers(0, 2**53, size=n, dtype=np.int64).astype(np.float64)
+    else:
+        rng = np.random.Generator(np.random.PCG64(11 if rank == 0 else [11, rank]))
+        r = np.minimum(rng.zipf(1.2, n), 2**53 - 1).astype(np.float64)
+        keys = (2.0**53 - 1) - r if dist == "zipf_hi" else r
+    return keys, np.arange(n, dtype=np.uint32)
 
 
 # ---- clocks (NVML, sampled during the timed region) --------------------------------
@@ -429,6 +440,7 @@ def run_b200(args, wl) -> None:
                                                                                   "t_post")}},
             "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(args.workload),
+                         "frac_of_nominal_8tbs": achieved / 8000.0,
                          "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": kms,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "fallback" not in peaks else "fallback"},
             "cpu_baseline": cpu,
@@ -450,6 +462,8 @@ def main() -> None:
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="join_c2")
     ap.add_argument("--k", type=int, default=None, help="override K for topk workloads")
+    ap.add_argument("--dist", choices=("uniform", "zipf_hi", "zipf_lo"), default="uniform",
+                    help="key distribution of the Top-K workloads")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every resident step eagerly")
     args = ap.parse_args()
@@ -458,6 +472,11 @@ def main() -> None:
     wl = dict(WORKLOADS[args.workload])
     if args.k is not None:
         wl["k"] = args.k
+    if args.dist != "uniform":
+        if wl["kind"] != "topk":
+            raise SystemExit("--dist applies to the Top-K workloads")
+        wl["dist"] = args.dist
+        wl["desc"] = wl["desc"].replace("uniform", args.dist.replace("_", "-") + " (SURVEY 8(d))")
     if args.impl == "reference":
         run_reference(args, wl)
     else:

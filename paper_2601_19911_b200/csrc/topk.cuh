@@ -637,15 +637,27 @@ __device__ __forceinline__ void filter_body(const double* __restrict__ keys, con
       if (vi < nv) v[u] = ldg_nc_d2(kv + 2 * vi);
       else v[u] = make_double2(-__longlong_as_double(0x7FF0000000000000ll), 0.0);
     }
-    unsigned flags = 0;
+    // keys above the threshold key are kept outright; keys equal to it (ties,
+    // e.g. a Zipf head) need their row: all those row loads go out together
+    unsigned flags = 0, ties = 0;
 #pragma unroll
     for (int u = 0; u < kFilterUnroll; ++u) {
       const uint64_t vi = wb + lane + (uint64_t)u * stride;
       if (vi < nv) {
-        const uint64_t p = head + 2 * vi;
-        if (filter_keep(v[u].x, tk, tr, rows, p)) flags |= 1u << (2 * u);
-        if (filter_keep(v[u].y, tk, tr, rows, p + 1)) flags |= 2u << (2 * u);
+        if (v[u].x > tk) flags |= 1u << (2 * u);
+        else if (v[u].x == tk) ties |= 1u << (2 * u);
+        if (v[u].y > tk) flags |= 2u << (2 * u);
+        else if (v[u].y == tk) ties |= 2u << (2 * u);
       }
+    }
+    if (ties) {
+      uint32_t rr[2 * kFilterUnroll];
+#pragma unroll
+      for (int e = 0; e < 2 * kFilterUnroll; ++e)
+        if ((ties >> e) & 1u) rr[e] = __ldg(rows + head + 2 * (wb + lane + (uint64_t)(e >> 1) * stride) + (e & 1));
+#pragma unroll
+      for (int e = 0; e < 2 * kFilterUnroll; ++e)
+        if (((ties >> e) & 1u) && rr[e] <= tr) flags |= 1u << e;
     }
     if (__any_sync(0xFFFFFFFFu, flags != 0)) {
 #pragma unroll
