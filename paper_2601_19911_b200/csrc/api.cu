@@ -705,11 +705,11 @@ int grid_for(uint64_t n, int threads, int per_sm) {
 }
 
 // Radix partitioning of the join (see join.cuh): slices of GOLP_JOIN_SLICE_BYTES
-// (default 16 MiB of slots) once the table exceeds two slices, at most
+// (default 32 MiB of slots) once the table exceeds two slices, at most
 // kMaxProbeParts slices.
 
 void plan_partitions(uint64_t cap) {
-  const uint64_t slice_bytes = std::max<uint64_t>(64, env_u64("GOLP_JOIN_SLICE_BYTES", 16ull << 20));
+  const uint64_t slice_bytes = std::max<uint64_t>(64, env_u64("GOLP_JOIN_SLICE_BYTES", 32ull << 20));
   uint64_t parts = 1;
   if (cap * sizeof(Slot) > 2 * slice_bytes) {
     while (parts < kMaxProbeParts && cap * sizeof(Slot) / parts > slice_bytes) parts <<= 1;
