@@ -16,7 +16,7 @@ PKG = HERE.parent
 ROOT = PKG.parent
 LIB = PKG / "libgolp_b200.so"
 SOURCES = ["api.cu", "host_engine.cpp", "runtime.cpp"]
-HEADERS = ["common.cuh", "sortnet.cuh", "topk.cuh", "join.cuh", "runtime.h"]
+HEADERS = ["common.cuh", "sortnet.cuh", "topk.cuh", "sort.cuh", "join.cuh", "runtime.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [
@@ -47,7 +47,7 @@ def _stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
     """Compile libgolp_b200.so (or a tuning variant with extra -D defines at `out`)."""
-    target = out or LIB
+    target = Path(out).resolve() if out is not None else LIB
     if not force and out is None and not defines and not _stale():
         return LIB
     nvcc = _nvcc()
