@@ -9,7 +9,7 @@
 //      skipped: a stable sort by key of row-ordered input is the lexsort order).
 //      Digits whose histogram is a single bucket are skipped too.
 //   2. one sort_pass_kernel per remaining digit ("onesweep"): a block claims the
-//      next tile, ranks its items stably per digit (warp match + per-warp digit
+//      next tile, ranks its items stably per digit (bit-plane ballots + per-warp digit
 //      counters), publishes the tile's digit counts and resolves its global digit
 //      offsets by decoupled look-back over earlier tiles, stages the tile in shared
 //      memory in digit order and writes each digit run contiguously. One read and
@@ -19,8 +19,17 @@
 
 namespace golp {
 
-constexpr int kSortThreads = 512;
-constexpr int kSortItems = 8;
+#ifndef GOLP_SORT_THREADS
+#define GOLP_SORT_THREADS 256
+#endif
+#ifndef GOLP_SORT_ITEMS
+#define GOLP_SORT_ITEMS 12
+#endif
+#ifndef GOLP_SORT_MINB
+#define GOLP_SORT_MINB 4
+#endif
+constexpr int kSortThreads = GOLP_SORT_THREADS;
+constexpr int kSortItems = GOLP_SORT_ITEMS;
 constexpr uint32_t kSortTileN = (uint32_t)kSortThreads * kSortItems;  // 2048 items
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortDigits = 12;
@@ -71,7 +80,7 @@ struct SortPassArgs {
   unsigned long long* tile_ctr;          // zeroed
 };
 
-__global__ void __launch_bounds__(kSortThreads, 2) sort_pass_kernel(SortPassArgs a) {
+__global__ void __launch_bounds__(kSortThreads, GOLP_SORT_MINB) sort_pass_kernel(SortPassArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* s_key = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* s_row = reinterpret_cast<uint32_t*>(s_key + kSortTileN);
