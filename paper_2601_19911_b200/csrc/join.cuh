@@ -434,9 +434,16 @@ __global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(unsigned lo
 // inside its tile plus the (offset, length) of every (tile, slice) run, so
 // join_unpartition_kernel can put results back in probe order tile by tile with
 // coalesced reads and writes (no scattered 8-byte stores).
-constexpr int kPartThreads = 512;
-constexpr int kPartItems = 8;
-constexpr uint32_t kPartTile = (uint32_t)kPartThreads * kPartItems;  // 4096 entries
+#ifndef GOLP_PART_THREADS
+#define GOLP_PART_THREADS 512
+#endif
+#ifndef GOLP_PART_MINB
+#define GOLP_PART_MINB 2
+#endif
+constexpr uint32_t kPartTile = 4096;  // entries per partition tile (run tables, match tiles)
+constexpr int kPartThreads = GOLP_PART_THREADS;
+constexpr int kPartItems = (int)(kPartTile / kPartThreads);
+static_assert(kPartItems * kPartThreads == (int)kPartTile && kPartItems % 2 == 0, "tile split");
 constexpr uint32_t kMaxParts = 1024;
 constexpr uint32_t kMaxProbeParts = 256;  // bounds the per-(tile, slice) run table
 constexpr size_t kPartSmem = (size_t)kPartTile * (8 + 2 + 2) + (size_t)kMaxParts * (4 + 4 + 8);
@@ -511,7 +518,7 @@ __device__ __forceinline__ void block_scan_parts(const unsigned* s_cnt, unsigned
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(const double* __restrict__ keys, uint64_t n,
+__global__ void __launch_bounds__(kPartThreads, GOLP_PART_MINB) part_scatter_kernel(const double* __restrict__ keys, uint64_t n,
                                                                     uint32_t mask, int slice_bits, uint32_t nparts,
                                                                     unsigned long long* __restrict__ cursors,
                                                                     PartOut out) {
