@@ -851,9 +851,9 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   CKL();
   join_finalize_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, brows, ga, cap * kInline);
   CKL();
-  join_overflow_kernel<<<g.sms * 2, 256, 0, s>>>(table, ga);
+  join_overflow_kernel<<<g.sms, 256, 0, s>>>(table, ga);
   CKL();
-  join_group_sort_kernel<<<g.sms, 128, 0, s>>>(table, ga, brows);
+  join_group_sort_kernel<<<std::max(1, g.sms / 2), 128, 0, s>>>(table, ga, brows);
   CKL();
   static bool attr = false;
   const size_t smem = kGroupTile * sizeof(uint32_t);
@@ -861,7 +861,7 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
     CK(cudaFuncSetAttribute(join_big_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  join_big_groups_kernel<<<g.sms, 1024, smem, s>>>(table, ga, brows);
+  join_big_groups_kernel<<<std::max(1, g.sms / 4), 1024, smem, s>>>(table, ga, brows);
   CKL();
   g_launches += 5;
   prof_record(5, s);
