@@ -936,12 +936,18 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
       const unsigned long long* bin = ci == 0 ? base_in : tmp + (ci & 1);
       unsigned long long* bout = last ? total_out : tmp + ((ci + 1) & 1);
       ++ci;
-      scan_partials_kernel<<<1, kScanThreads, 0, s>>>(part, (uint32_t)blocks, bin, bout);
+      if (blocks <= kInlineScanBlocks) {  // emit blocks add up the earlier blocks' totals themselves
+        join_emit_kernel<false><<<(unsigned)blocks, kProbeThreads, 0, s>>>(
+            sc, g.rows_arr.as<uint32_t>(), nwt, per_warp, part, bin, bout, out_p, out_b, cap);
+      } else {
+        scan_partials_kernel<<<1, kScanThreads, 0, s>>>(part, (uint32_t)blocks, bin, bout);
+        CKL();
+        ++g_launches;
+        join_emit_kernel<true><<<(unsigned)blocks, kProbeThreads, 0, s>>>(
+            sc, g.rows_arr.as<uint32_t>(), nwt, per_warp, part, bin, bout, out_p, out_b, cap);
+      }
       CKL();
-      join_emit_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(sc, g.rows_arr.as<uint32_t>(), nwt, per_warp,
-                                                                  part, out_p, out_b, cap);
-      CKL();
-      g_launches += 3;
+      g_launches += 2;
     }
   }
   return GOLP_OK;

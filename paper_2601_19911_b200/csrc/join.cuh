@@ -883,22 +883,45 @@ __global__ void __launch_bounds__(kProbeThreads) join_match_runs_kernel(
   finish_match_block(lane, warp, gw, lo, cursor, pairs_total, sc, s_w, bpart);
 }
 
-// Same block/warp -> tile mapping as join_match_kernel. bpart holds the exclusive
-// offsets of the blocks (scan_partials_kernel); a warp's offset adds the pairs of
-// the earlier warps of its block. Singletons (slot.off is the build row) are a
-// straight coalesced copy; key groups expand their CSR run.
+// Same block/warp -> tile mapping as join_match_kernel. bpart holds the pair
+// totals of the match blocks. With few blocks (kScanned = false) each emit block
+// sums the totals of the blocks before it (at most a few thousand L2-resident
+// words) on top of *base_in, so no separate scan launch is needed, and the last
+// block writes *total_out; with many, scan_partials_kernel has already turned
+// bpart into exclusive offsets. A warp's offset adds the pairs of the earlier
+// warps of its block. Singletons (slot.off is the build row) are a straight
+// coalesced copy; key groups expand their CSR run.
+constexpr uint64_t kInlineScanBlocks = 4096;
+template <bool kScanned>
 __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch sc, const uint32_t* __restrict__ csr_row,
                                                                   uint64_t nwt, uint64_t per_warp,
                                                                   const unsigned long long* __restrict__ bpart,
+                                                                  const unsigned long long* __restrict__ base_in,
+                                                                  unsigned long long* __restrict__ total_out,
                                                                   uint32_t* __restrict__ out_p,
                                                                   uint32_t* __restrict__ out_b, uint64_t cap) {
   __shared__ unsigned long long s_wp[kProbeWarps];
+  __shared__ unsigned long long s_red[kProbeWarps];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint64_t gw = (uint64_t)blockIdx.x * kProbeWarps + warp;
+  if constexpr (!kScanned) {  // exclusive offset of this block: sum of the earlier blocks' totals
+    unsigned long long acc = 0;
+    for (unsigned b = threadIdx.x; b < blockIdx.x; b += blockDim.x) acc += __ldcg(bpart + b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if (lane == 0) s_red[warp] = acc;
+  }
   const uint64_t lo = gw * per_warp;
   if (lane == 0) s_wp[warp] = lo < nwt ? sc.wpairs[gw] : 0ull;
   __syncthreads();
-  unsigned long long run = bpart[blockIdx.x];
+  unsigned long long run;
+  if constexpr (kScanned) {
+    run = bpart[blockIdx.x];
+  } else {
+    run = *base_in;
+    for (unsigned w = 0; w < kProbeWarps; ++w) run += s_red[w];
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total_out = run + __ldcg(bpart + blockIdx.x);
+  }
   for (unsigned w = 0; w < warp; ++w) run += s_wp[w];
   if (lo >= nwt) return;
   const uint64_t pol_stream = policy_evict_first();
