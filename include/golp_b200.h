@@ -80,6 +80,16 @@ int golp_init(int device, uint64_t pinned_chunk_bytes, int host_threads);
 int golp_shutdown(void);
 /* Number of CUDA kernels this library has launched (process lifetime). */
 uint64_t golp_launch_count(void);
+/* Bytes the copy engines actually moved during the last host-buffer call
+ * (golp_topk / golp_probe [+ golp_probe_copy_out] / golp_full_sort). The
+ * ledger's h2d_bytes / d2h_bytes keep the reference's shape formulas
+ * (device.py:372-379, 428-435); these can be lower, because a dense row-id
+ * column (rows[i] == rows[0] + i, extract_keys's arange, store.py:178-181) is
+ * verified on the host and regenerated on the device instead of copied. */
+int golp_last_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+/* 1 (default; env GOLP_DENSE_ROWS=0 turns it off): dense row-id columns are
+ * regenerated on the device; 0: every row-id column is copied. */
+int golp_set_dense_rows(int on);
 int golp_set_profiling(int on);
 int golp_last_kernel_times(golp_kernel_times* out);
 

@@ -67,6 +67,8 @@ SIGNATURES = {
     "golp_init": (_int, [_int, _u64, _int]),
     "golp_shutdown": (_int, []),
     "golp_launch_count": (_u64, []),
+    "golp_last_transfer": (_int, [C.POINTER(_u64), C.POINTER(_u64)]),
+    "golp_set_dense_rows": (_int, [_int]),
     "golp_set_profiling": (_int, [_int]),
     "golp_last_kernel_times": (_int, [C.POINTER(KernelTimes)]),
     "golp_topk": (_int, [_vp, _vp, _u64, _u64, _int, _u32, _vp, C.POINTER(_u64), C.POINTER(Ledger)]),
@@ -175,6 +177,14 @@ _keepalive: dict = {}
 
 def launch_count() -> int:
     return int(load().golp_launch_count())
+
+
+def last_transfer() -> tuple:
+    """(h2d_bytes, d2h_bytes) the copy engines actually moved during the last
+    host-buffer call (a dense row-id column is regenerated on the device, not copied)."""
+    h2d, d2h = _u64(0), _u64(0)
+    check(load().golp_last_transfer(C.byref(h2d), C.byref(d2h)))
+    return int(h2d.value), int(d2h.value)
 
 
 def kernel_times() -> dict:

@@ -120,6 +120,10 @@ struct Ctx {
   int jslice_bits = 0;
   uint64_t last_m = 0;
   bool last_probe_valid = false;
+  // Bytes the copy engines actually moved for the current / last host-buffer
+  // call (the ledger keeps the reference's shape formulas instead).
+  uint64_t moved_h2d = 0, moved_d2h = 0;
+  bool dense_rows = true;  // GOLP_DENSE_ROWS=0 ships every row-id column
 
   char* status_host = nullptr;  // mapped pinned words: select status + candidate count
   char* status_dev = nullptr;
@@ -163,6 +167,7 @@ int do_init(int device, uint64_t chunk_bytes, int host_threads) {
   int hw = (int)std::thread::hardware_concurrency();
   if (host_threads <= 0) host_threads = std::max(1, std::min(4, hw - 1));
   g.pool.start(host_threads);
+  if (const char* v = getenv("GOLP_DENSE_ROWS")) g.dense_rows = std::atoi(v) != 0;
   CK(g.ctl.ensure(sizeof(SelectCtl) * kNumCtl));
   g.ready = true;
   return GOLP_OK;
@@ -198,6 +203,7 @@ bool is_pinned(const void* p) {
 // Host -> device copy of an arbitrary pageable buffer: the pool packs chunk i+1
 // into a pinned slot while the DMA engine drains chunk i.
 int stage_h2d(void* dst, const void* src, size_t bytes) {
+  g.moved_h2d += bytes;
   if (bytes && is_pinned(src)) {  // page-locked source: no host copy
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g.s_h2d));
     return GOLP_OK;
@@ -217,10 +223,35 @@ int stage_h2d(void* dst, const void* src, size_t bytes) {
   return GOLP_OK;
 }
 
+__global__ void fill_dense_rows_kernel(uint32_t* __restrict__ dst, uint32_t base, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = base + (uint32_t)i;
+}
+
+// Row-id column upload. A dense run (rows[i] == rows[0] + i, which is what
+// extract_keys produces, pkg/src/golp/store.py:178-181) does not cross PCIe:
+// the pool verifies it on the host while the key column queued just before it
+// is in flight, and a fill kernel on the copy stream writes it in HBM (stream
+// order = the same events as a copy). Any other column is copied as is. The
+// device therefore sees exactly the caller's row ids either way.
+int upload_rows(uint32_t* dst, const uint32_t* src, uint64_t n) {
+  if (!n) return GOLP_OK;
+  if (g.dense_rows && dense_run(g.pool, src, n)) {
+    const int grid = (int)std::min<uint64_t>((n + 1023) / 1024, (uint64_t)g.sms * 8);
+    fill_dense_rows_kernel<<<grid, 256, 0, g.s_h2d>>>(dst, src[0], n);
+    CKL();
+    ++g_launches;
+    return GOLP_OK;
+  }
+  return stage_h2d(dst, src, n * 4);
+}
+
 // Full-row mode ships payload bytes the device never reads: stream a pinned slot
 // (contents irrelevant) into a device scratch chunk, repeatedly.
 int stage_dummy_h2d(size_t bytes) {
   if (!bytes) return GOLP_OK;
+  g.moved_h2d += bytes;
   CK(g.in_payload.ensure(g.chunk));
   size_t done = 0;
   while (done < bytes) {
@@ -251,6 +282,7 @@ int d2h_complete_one() {
 }
 
 int d2h_enqueue(void* dst, const void* src, size_t bytes) {
+  g.moved_d2h += bytes;
   if (bytes && is_pinned(dst)) {  // page-locked destination (result arena): no host copy
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g.s_d2h));
     g.d2h_direct = true;
@@ -1147,6 +1179,19 @@ int golp_shutdown(void) {
 
 uint64_t golp_launch_count(void) { return g_launches.load(); }
 
+int golp_set_dense_rows(int on) {
+  RET(ensure_init());
+  g.dense_rows = on != 0;
+  return GOLP_OK;
+}
+
+int golp_last_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
+  if (!h2d_bytes || !d2h_bytes) return invalid("null output pointer");
+  *h2d_bytes = g.moved_h2d;
+  *d2h_bytes = g.moved_d2h;
+  return GOLP_OK;
+}
+
 int golp_set_profiling(int on) {
   RET(ensure_init());
   g.prof = on != 0;
@@ -1207,6 +1252,7 @@ int golp_full_sort(const double* keys, const uint32_t* rows, uint64_t n, int mod
   RET(check_mode(mode, payload_bytes, &entry));
   if (!led) return invalid("null ledger");
   RET(ensure_init());
+  g.moved_h2d = g.moved_d2h = 0;
   const double t0 = wall_seconds();
   *led = golp_ledger{entry * n, 4 * n, 0.0, 0.0, 0.0, 0.0};
   if (n == 0) return GOLP_OK;
@@ -1216,7 +1262,7 @@ int golp_full_sort(const double* keys, const uint32_t* rows, uint64_t n, int mod
   CK(g.in_rows.ensure(n * 4));
   CK(g.out_rows.ensure(n * 4));
   RET(stage_h2d(g.in_keys.p, keys, n * 8));
-  RET(stage_h2d(g.in_rows.p, rows, n * 4));
+  RET(upload_rows(g.in_rows.as<uint32_t>(), rows, n));
   if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(n * (size_t)payload_bytes));
   cudaEvent_t ev_up = g.ev[2];
   CK(cudaEventRecord(ev_up, g.s_h2d));
@@ -1231,6 +1277,7 @@ int golp_full_sort(const double* keys, const uint32_t* rows, uint64_t n, int mod
   const double t2 = wall_seconds();
   if (is_pinned(out_rows)) {
     CK(cudaMemcpyAsync(out_rows, g.out_rows.p, n * 4, cudaMemcpyDeviceToHost, g.s_d2h));
+    g.moved_d2h += n * 4;
     CK(cudaStreamSynchronize(g.s_d2h));
   } else {
     RET(stage_d2h(out_rows, g.out_rows.p, n * 4));
@@ -1302,6 +1349,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
   RET(check_mode(mode, payload_bytes, &entry));
   if (!out_len || !led) return invalid("null output pointer");
   RET(ensure_init());
+  g.moved_h2d = g.moved_d2h = 0;
   const double t0 = wall_seconds();
   const uint64_t kk = std::min(k, n);
   *out_len = kk;
@@ -1327,7 +1375,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     const bool trace = std::getenv("GOLP_TRACE") != nullptr;
     RET(stage_h2d(dk, keys, n * 8));
     if (trace) std::fprintf(stderr, "[golp] topk %.3f ms keys queued\n", (wall_seconds() - t0) * 1e3);
-    RET(stage_h2d(dr, rows, n * 4));
+    RET(upload_rows(dr, rows, n));
     if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(n * (size_t)payload_bytes));
     CK(cudaEventRecord(ev_chunk, g.s_h2d));
     if (trace) std::fprintf(stderr, "[golp] topk %.3f ms rows queued\n", (wall_seconds() - t0) * 1e3);
@@ -1343,6 +1391,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     const double t2 = wall_seconds();
     uint32_t* hbuf = static_cast<uint32_t*>(g.pin_small);
     CK(cudaMemcpyAsync(hbuf, d_out, kk * 4, cudaMemcpyDeviceToHost, s));
+    g.moved_d2h += kk * 4;
     CK(cudaStreamSynchronize(s));
     std::memcpy(out_rows, hbuf, kk * 4);
     led->t_h2d = t1 - t0;
@@ -1366,6 +1415,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     uint32_t* dsr = reinterpret_cast<uint32_t*>(ds + p.s);
     CK(cudaMemcpyAsync(ds, hs, p.s * 8, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dsr, hr, p.s * 4, cudaMemcpyHostToDevice, s));
+    g.moved_h2d += p.s * 12;
     CK(cudaMemsetAsync(ctl(0), 0, sizeof(SelectCtl) * 2, s));
     RET(launch_select(make_args(SrcInput{ds, dsr}, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), s));
   }
@@ -1373,7 +1423,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
   for (uint64_t c0 = 0; c0 < n; c0 += per_chunk) {
     const uint64_t cn = std::min(per_chunk, n - c0);
     RET(stage_h2d(dk + c0, keys + c0, cn * 8));
-    RET(stage_h2d(dr + c0, rows + c0, cn * 4));
+    RET(upload_rows(dr + c0, rows + c0, cn));
     if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(cn * (size_t)payload_bytes));
     if (!p.direct) {
       CK(cudaEventRecord(ev_chunk, g.s_h2d));
@@ -1408,6 +1458,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
   uint32_t* hbuf = static_cast<uint32_t*>(g.pin_small);
   if (kk * 4 <= g.pin_small_bytes) {
     CK(cudaMemcpyAsync(hbuf, d_out, kk * 4, cudaMemcpyDeviceToHost, s));
+    g.moved_d2h += kk * 4;
     CK(cudaStreamSynchronize(s));
     std::memcpy(out_rows, hbuf, kk * 4);
   } else {
@@ -1430,6 +1481,7 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   if (out_cap && (!out_probe_rows || !out_build_rows)) return invalid("null output arrays");
   RET(ensure_init());
   g.last_probe_valid = false;
+  g.moved_h2d = g.moved_d2h = 0;
   const double t0 = wall_seconds();
   *led = golp_ledger{entry * (nb + np), 0, 0.0, 0.0, 0.0, 0.0};
   *out_matches = 0;
@@ -1446,7 +1498,7 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
 
   // build side first, then the probe side in chunks that are probed as they land
   RET(stage_h2d(dbk, build_keys, nb * 8));
-  RET(stage_h2d(dbr, build_rows, nb * 4));
+  RET(upload_rows(dbr, build_rows, nb));
   if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(nb * (size_t)payload_bytes));
   cudaEvent_t ev_chunk = g.ev[0];
   CK(cudaEventRecord(ev_chunk, g.s_h2d));
@@ -1518,7 +1570,7 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
           }
         }
         RET(stage_h2d(dpk + c0, probe_keys + c0, cn * 8));
-        RET(stage_h2d(dpr + c0, probe_rows + c0, cn * 4));
+        RET(upload_rows(dpr + c0, probe_rows + c0, cn));
         if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(cn * (size_t)payload_bytes));
         CK(cudaEventRecord(g.h2d_ev[c], g.s_h2d));
         CK(cudaStreamWaitEvent(s, g.h2d_ev[c], 0));

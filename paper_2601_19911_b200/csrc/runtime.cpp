@@ -89,4 +89,30 @@ void parallel_copy(WorkerPool& pool, void* dst, const void* src, size_t bytes) {
   });
 }
 
+bool dense_run(WorkerPool& pool, const uint32_t* src, size_t n) {
+  if (n < 2) return true;
+  const uint32_t base = src[0];
+  // Permuted or shifted columns fail here without touching the rest.
+  if (src[1] != base + 1u || src[n - 1] != base + (uint32_t)(n - 1) || src[n / 2] != base + (uint32_t)(n / 2))
+    return false;
+  constexpr size_t kPiece = size_t(1) << 18;  // 1 MB of row ids per task
+  const size_t tasks = (n + kPiece - 1) / kPiece;
+  std::atomic<bool> ok{true};
+  auto check = [&](size_t t) {
+    if (!ok.load(std::memory_order_relaxed)) return;
+    const size_t lo = t * kPiece, hi = std::min(n, lo + kPiece);
+    uint32_t bad = 0;
+    uint32_t want = base + (uint32_t)lo;
+    for (size_t i = lo; i < hi; ++i, ++want) bad |= src[i] ^ want;
+    if (bad) ok.store(false, std::memory_order_relaxed);
+  };
+  if (tasks <= 1 || pool.size() == 0) {
+    for (size_t t = 0; t < tasks; ++t) check(t);
+  } else {
+    pool.run(tasks, check);
+  }
+  return ok.load();
+}
+
 }  // namespace golp
+

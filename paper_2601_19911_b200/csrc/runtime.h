@@ -43,4 +43,9 @@ class WorkerPool {
 // memcpy split across the pool (the packer's inner loop).
 void parallel_copy(WorkerPool& pool, void* dst, const void* src, size_t bytes);
 
+// True when src[i] == src[0] + i (mod 2^32) for every i < n: a dense row-id run
+// such as extract_keys's arange (pkg/src/golp/store.py:178-181). Split across
+// the pool, stops at the first mismatch.
+bool dense_run(WorkerPool& pool, const uint32_t* src, size_t n);
+
 }  // namespace golp
