@@ -107,6 +107,7 @@ struct Ctx {
   size_t pin_small_bytes = 16u << 20;
   WorkerPool pool;
   cudaEvent_t ev[8] = {};
+  cudaEvent_t ev_rows = nullptr;  // a copied row column of a chunked upload has landed
 
   DevBuf ctl, cand_hi, cand_lo, w_hi, w_lo, out_rows, out_hi, samples;
   DevBuf table, rows_arr, ovf, big_list, jcount, wcount, partial, totals, totals2;
@@ -164,6 +165,7 @@ int do_init(int device, uint64_t chunk_bytes, int host_threads) {
   }
   CK(cudaHostAlloc(&g.pin_small, g.pin_small_bytes, cudaHostAllocDefault));
   for (auto& e : g.ev) CK(cudaEventCreate(&e));
+  CK(cudaEventCreateWithFlags(&g.ev_rows, cudaEventDisableTiming));
   int hw = (int)std::thread::hardware_concurrency();
   if (host_threads <= 0) host_threads = std::max(1, std::min(4, hw - 1));
   g.pool.start(host_threads);
@@ -232,18 +234,26 @@ __global__ void fill_dense_rows_kernel(uint32_t* __restrict__ dst, uint32_t base
 // Row-id column upload. A dense run (rows[i] == rows[0] + i, which is what
 // extract_keys produces, pkg/src/golp/store.py:178-181) does not cross PCIe:
 // the pool verifies it on the host while the key column queued just before it
-// is in flight, and a fill kernel on the copy stream writes it in HBM (stream
-// order = the same events as a copy). Any other column is copied as is. The
+// is in flight, and a fill kernel writes it in HBM on the main stream, where
+// every consumer of the column runs (on the copy stream it would hold back the
+// next upload until it finished). Any other column is copied as is. The
 // device therefore sees exactly the caller's row ids either way.
-int upload_rows(uint32_t* dst, const uint32_t* src, uint64_t n) {
+int upload_rows(uint32_t* dst, const uint32_t* src, uint64_t n, bool* copied = nullptr) {
+  if (copied) *copied = false;
   if (!n) return GOLP_OK;
-  if (g.dense_rows && dense_run(g.pool, src, n)) {
+  const double tv = wall_seconds();
+  const bool dense = g.dense_rows && dense_run(g.pool, src, n);
+  if (std::getenv("GOLP_TRACE"))
+    std::fprintf(stderr, "[golp] rows [%llu] verified in %.3f ms: %s\n", (unsigned long long)n, (wall_seconds() - tv) * 1e3,
+                 dense ? "dense" : "copied");
+  if (dense) {
     const int grid = (int)std::min<uint64_t>((n + 1023) / 1024, (uint64_t)g.sms * 8);
-    fill_dense_rows_kernel<<<grid, 256, 0, g.s_h2d>>>(dst, src[0], n);
+    fill_dense_rows_kernel<<<grid, 256, 0, g.s_main>>>(dst, src[0], n);
     CKL();
     ++g_launches;
     return GOLP_OK;
   }
+  if (copied) *copied = true;
   return stage_h2d(dst, src, n * 4);
 }
 
@@ -1168,6 +1178,8 @@ int golp_shutdown(void) {
     if (e) cudaEventDestroy(e);
     e = nullptr;
   }
+  if (g.ev_rows) cudaEventDestroy(g.ev_rows);
+  g.ev_rows = nullptr;
   cudaStreamDestroy(g.s_main);
   cudaStreamDestroy(g.s_h2d);
   cudaStreamDestroy(g.s_d2h);
@@ -1420,17 +1432,34 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     RET(launch_select(make_args(SrcInput{ds, dsr}, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), s));
   }
   // Stream the columns chunk by chunk; filter each chunk as soon as it lands.
-  for (uint64_t c0 = 0; c0 < n; c0 += per_chunk) {
-    const uint64_t cn = std::min(per_chunk, n - c0);
-    RET(stage_h2d(dk + c0, keys + c0, cn * 8));
-    RET(upload_rows(dr + c0, rows + c0, cn));
+  // The rows of chunk c are verified (or copied) after the keys of chunk c+1
+  // are queued, so the copy engine has the next upload while the pool reads.
+  // h2d_ev[c] fires when the keys of chunk c have landed; a copied row column
+  // (or full-row payload) adds a second event after the next chunk's keys.
+  const uint64_t nchunks = (n + per_chunk - 1) / per_chunk;
+  RET(ensure_chunk_events(nchunks));
+  auto finish_chunk = [&](uint64_t c) -> int {
+    const uint64_t c0 = c * per_chunk, cn = std::min(per_chunk, n - c0);
+    bool copied = false;
+    RET(upload_rows(dr + c0, rows + c0, cn, &copied));
     if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(cn * (size_t)payload_bytes));
     if (!p.direct) {
-      CK(cudaEventRecord(ev_chunk, g.s_h2d));
-      CK(cudaStreamWaitEvent(s, ev_chunk, 0));
+      CK(cudaStreamWaitEvent(s, g.h2d_ev[c], 0));
+      if (copied || mode == GOLP_FULL_ROW) {
+        CK(cudaEventRecord(ev_chunk, g.s_h2d));
+        CK(cudaStreamWaitEvent(s, ev_chunk, 0));
+      }
       RET(launch_filter(dk + c0, dr + c0, cn, p.cap, s));
     }
+    return GOLP_OK;
+  };
+  for (uint64_t c = 0; c < nchunks; ++c) {
+    const uint64_t c0 = c * per_chunk;
+    RET(stage_h2d(dk + c0, keys + c0, std::min(per_chunk, n - c0) * 8));
+    CK(cudaEventRecord(g.h2d_ev[c], g.s_h2d));
+    if (c) RET(finish_chunk(c - 1));
   }
+  RET(finish_chunk(nchunks - 1));
   CK(cudaEventRecord(ev_chunk, g.s_h2d));
   CK(cudaEventSynchronize(ev_chunk));
   g.next_slot = 0;
@@ -1496,9 +1525,26 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   double* dpk = g.in_keys.as<double>();
   uint32_t* dpr = g.in_rows.as<uint32_t>();
 
+  // GOLP_TRACE: per-upload host queue times and device completion times
+  const bool trace = std::getenv("GOLP_TRACE") != nullptr;
+  static std::vector<cudaEvent_t> tr_ev;
+  std::vector<double> tr_q;
+  auto tr_mark = [&]() -> int {
+    if (!trace) return GOLP_OK;
+    if (tr_ev.size() <= tr_q.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      tr_ev.push_back(e);
+    }
+    CK(cudaEventRecord(tr_ev[tr_q.size()], g.s_h2d));
+    tr_q.push_back((wall_seconds() - t0) * 1e3);
+    return GOLP_OK;
+  };
+  RET(tr_mark());
   // build side first, then the probe side in chunks that are probed as they land
   RET(stage_h2d(dbk, build_keys, nb * 8));
   RET(upload_rows(dbr, build_rows, nb));
+  RET(tr_mark());
   if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(nb * (size_t)payload_bytes));
   cudaEvent_t ev_chunk = g.ev[0];
   CK(cudaEventRecord(ev_chunk, g.s_h2d));
@@ -1507,7 +1553,21 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
 
   uint64_t per_chunk = std::max<uint64_t>(g.chunk / 8, kWarpTile);
   per_chunk = (per_chunk / kWarpTile) * kWarpTile;
-  const uint64_t nchunks = np ? (np + per_chunk - 1) / per_chunk : 0;
+  // Chunk bounds: full staging chunks, then the last chunk's worth of probes in
+  // kTailSplit pieces, so the work left after the final upload (its probe and
+  // its pairs' download) is a fraction of a chunk.
+  constexpr uint64_t kTailSplit = 4;
+  std::vector<uint64_t> cb{0};
+  while (cb.back() < np) {
+    const uint64_t left = np - cb.back();
+    uint64_t len = per_chunk;
+    if (left <= per_chunk) {
+      len = std::max<uint64_t>(((per_chunk / kTailSplit) / kWarpTile) * kWarpTile, kWarpTile);
+      if (left < 2 * len) len = left;
+    }
+    cb.push_back(cb.back() + std::min(len, left));
+  }
+  const uint64_t nchunks = cb.size() - 1;
   CK(g.totals.ensure((nchunks + 1) * 8));
   CK(cudaMemsetAsync(g.totals.p, 0, (nchunks + 1) * 8, s));
   RET(ensure_chunk_events(nchunks));
@@ -1527,7 +1587,6 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   // later chunks upload; a chunk is ready once its probe event has fired.
   uint64_t streamed = 0;     // chunks whose pairs are queued for D2H
   bool streaming = out_cap > 0;
-  const bool trace = std::getenv("GOLP_TRACE") != nullptr;
   auto stream_ready = [&](bool block) -> int {
     while (streaming && streamed < nchunks) {
       cudaEvent_t e = g.chunk_ev[streamed];
@@ -1553,35 +1612,62 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
     }
     return d2h_poll();
   };
+  // The rows of chunk c are verified (or copied) after the keys of chunk c+1
+  // are queued, so the copy engine has the next upload while the pool reads.
+  // h2d_ev[c] fires when the keys of chunk c have landed; a copied row column
+  // (or full-row payload) adds a second event after the next chunk's keys.
+  auto finish_upload = [&](uint64_t c) -> int {
+    const uint64_t c0 = cb[c], cn = cb[c + 1] - c0;
+    bool copied = false;
+    RET(upload_rows(dpr + c0, probe_rows + c0, cn, &copied));
+    if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(cn * (size_t)payload_bytes));
+    CK(cudaStreamWaitEvent(s, g.h2d_ev[c], 0));
+    if (copied || mode == GOLP_FULL_ROW) {
+      CK(cudaEventRecord(g.ev_rows, g.s_h2d));
+      CK(cudaStreamWaitEvent(s, g.ev_rows, 0));
+    }
+    return GOLP_OK;
+  };
+  auto probe_chunk = [&](uint64_t c, uint32_t* op, uint32_t* ob, uint64_t cap_) -> int {
+    const uint64_t c0 = cb[c], cn = cb[c + 1] - c0;
+    RET(launch_probe(dpk + c0, dpr + c0, cn, op, ob, cap_, totals + c, totals + c + 1, s));
+    publish_u64_kernel<<<1, 1, 0, s>>>(reinterpret_cast<volatile unsigned long long*>(g.mirror_dev + c + 1),
+                                       totals + c + 1);
+    CKL();
+    ++g_launches;
+    CK(cudaEventRecord(g.chunk_ev[c], s));
+    return GOLP_OK;
+  };
   auto run_chunks = [&](bool with_h2d, uint32_t* op, uint32_t* ob, uint64_t cap_) -> int {
+    if (!with_h2d) {
+      for (uint64_t c = 0; c < nchunks; ++c) RET(probe_chunk(c, op, ob, cap_));
+      return GOLP_OK;
+    }
     for (uint64_t c = 0; c < nchunks; ++c) {
-      const uint64_t c0 = c * per_chunk;
-      const uint64_t cn = std::min(per_chunk, np - c0);
-      if (with_h2d) {
-        // Keep at most two chunks of uploads in flight: copies are serviced in
-        // submission order, so pair downloads queued in between can overlap them.
-        if (c >= 2) {
-          while (true) {
-            const cudaError_t q = cudaEventQuery(g.h2d_ev[c - 2]);
-            if (q == cudaSuccess) break;
-            if (q != cudaErrorNotReady) CK(q);
-            RET(stream_ready(false));
-            std::this_thread::yield();
-          }
+      // Keep at most two chunks of uploads in flight: copies are serviced in
+      // submission order, so pair downloads queued in between can overlap them.
+      if (c >= 2) {
+        while (true) {
+          const cudaError_t q = cudaEventQuery(g.h2d_ev[c - 2]);
+          if (q == cudaSuccess) break;
+          if (q != cudaErrorNotReady) CK(q);
+          RET(stream_ready(false));
+          std::this_thread::yield();
         }
-        RET(stage_h2d(dpk + c0, probe_keys + c0, cn * 8));
-        RET(upload_rows(dpr + c0, probe_rows + c0, cn));
-        if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(cn * (size_t)payload_bytes));
-        CK(cudaEventRecord(g.h2d_ev[c], g.s_h2d));
-        CK(cudaStreamWaitEvent(s, g.h2d_ev[c], 0));
       }
-      RET(launch_probe(dpk + c0, dpr + c0, cn, op, ob, cap_, totals + c, totals + c + 1, s));
-      publish_u64_kernel<<<1, 1, 0, s>>>(reinterpret_cast<volatile unsigned long long*>(g.mirror_dev + c + 1),
-                                         totals + c + 1);
-      CKL();
-      ++g_launches;
-      CK(cudaEventRecord(g.chunk_ev[c], s));
-      if (with_h2d) RET(stream_ready(false));
+      RET(stage_h2d(dpk + cb[c], probe_keys + cb[c], (cb[c + 1] - cb[c]) * 8));
+      RET(tr_mark());
+      CK(cudaEventRecord(g.h2d_ev[c], g.s_h2d));
+      if (c > 0) {
+        RET(finish_upload(c - 1));
+        RET(probe_chunk(c - 1, op, ob, cap_));
+        RET(stream_ready(false));
+      }
+    }
+    if (nchunks) {
+      RET(finish_upload(nchunks - 1));
+      RET(probe_chunk(nchunks - 1, op, ob, cap_));
+      RET(stream_ready(false));
     }
     return GOLP_OK;
   };
@@ -1639,7 +1725,14 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   RET(stream_ready(true));
   RET(d2h_flush());
   const double t3 = wall_seconds();
-  if (trace) std::fprintf(stderr, "[golp] %.3f ms pairs landed\n", (t3 - t0) * 1e3);
+  if (trace) {
+    std::fprintf(stderr, "[golp] %.3f ms pairs landed\n", (t3 - t0) * 1e3);
+    for (size_t i = 1; i < tr_q.size(); ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, tr_ev[0], tr_ev[i]));
+      std::fprintf(stderr, "[golp]   upload %zu: queued at %.3f ms, landed %.3f ms after the first queue\n", i - 1, tr_q[i], ms);
+    }
+  }
   *out_matches = m;
   g.last_m = m;
   g.last_probe_valid = true;  // copy_out reads the device pair buffers
