@@ -197,3 +197,46 @@ def test_partitioned_join_natural_scale(cuda):
     ep, eb = oracle.join(bk, br, pk, pr)
     assert np.array_equal(op.cpu().numpy().view(np.uint32), ep)
     assert np.array_equal(ob.cpu().numpy().view(np.uint32), eb)
+
+
+def _mix64(z):
+    z = z.astype(np.uint64)
+    z ^= z >> np.uint64(30)
+    z *= np.uint64(0xBF58476D1CE4E5B9)
+    z ^= z >> np.uint64(27)
+    z *= np.uint64(0x94D049BB133111EB)
+    z ^= z >> np.uint64(31)
+    return z
+
+
+@pytest.mark.parametrize("where", ["slice_end", "table_end", "one_slice_overfull"])
+def test_probe_keys_crowding_a_slice_boundary(b200, where):
+    """Build keys chosen (through mix64) to crowd a few home slots -- at the end
+    of a 2048-slot region, at the end of the table (walks wrap to slot 0), or
+    2600 keys homed in one quarter of the table: long linear-probing walks, and
+    groups of up to ~60 members exercise every group path."""
+    nb_rand = 3000
+    cap = 8192  # pow2 >= 2 * nb for nb in (2048, 4096]
+    cand = np.arange(1, 3_000_000, dtype=np.float64)
+    home = (_mix64(cand.view(np.uint64)) & np.uint64(cap - 1)) & ~np.uint64(1)
+    if where == "slice_end":
+        pick = cand[(home >= 2048 - 8) & (home < 2048)][:120]
+    elif where == "table_end":
+        pick = cand[home >= cap - 8][:120]
+    else:  # far more keys than a 2048-slot slice holds
+        pick = cand[home < 2048][:2600]
+    rng = np.random.default_rng(len(pick))
+    reps = rng.integers(1, 60, size=len(pick)) if where != "one_slice_overfull" else np.ones(len(pick), np.int64)
+    crowd = np.repeat(pick, reps)
+    nb = min(len(crowd), 4000)
+    filler = rng.integers(5_000_000, 6_000_000, size=max(0, 4000 - nb)).astype(np.float64)
+    bk = rng.permutation(np.concatenate([crowd[:nb], filler]))
+    assert 2048 < len(bk) <= 4096
+    br = rng.permutation(len(bk)).astype(np.uint32)
+    pk = np.concatenate([pick, filler[:500], rng.integers(0, 7_000_000, size=3000).astype(np.float64)])
+    pk = rng.permutation(pk)
+    pr = np.arange(len(pk), dtype=np.uint32)
+    res = b200.probe(KeyVector(bk, br), KeyVector(pk, pr))
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert res.payload.match_count == len(ep)
+    assert np.array_equal(res.payload.probe_rows, ep) and np.array_equal(res.payload.build_rows, eb)
