@@ -749,9 +749,21 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_ker
 // slot of keys[i] (0 when absent), in partitioned order. Blocks claim chunks of
 // kPartProbeSub sub-tiles in order (TileSched); inside a chunk the keys of the
 // next sub-tile are loaded while the current one's lookups are in flight.
-constexpr int kPartProbeItems = 4;
-constexpr int kPartProbeSub = 8;
-__global__ void __launch_bounds__(kProbeThreads, 3) join_probe_part_kernel(const double* __restrict__ keys, uint64_t n,
+// One lookup per thread at full occupancy (8 blocks of 256, 30 registers) beat
+// 4 per thread at 3 blocks/SM (80 registers): 27.4 vs 30.3 ms for a 1.07e9-probe
+// span against the C4 table (tools/part_probe_variants.py).
+#ifndef GOLP_PART_PROBE_ITEMS
+#define GOLP_PART_PROBE_ITEMS 1
+#endif
+#ifndef GOLP_PART_PROBE_MINB
+#define GOLP_PART_PROBE_MINB 8
+#endif
+constexpr int kPartProbeItems = GOLP_PART_PROBE_ITEMS;
+#ifndef GOLP_PART_PROBE_SUB
+#define GOLP_PART_PROBE_SUB 8
+#endif
+constexpr int kPartProbeSub = GOLP_PART_PROBE_SUB;
+__global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_probe_part_kernel(const double* __restrict__ keys, uint64_t n,
                                                                         const Slot* __restrict__ table, uint64_t mask,
                                                                         uint64_t* __restrict__ res_part,
                                                                         int table_policy, TileSched sched) {
