@@ -466,9 +466,30 @@ def run_b200(args, wl) -> None:
         }
         if wl["kind"] == "join":
             line["roofline"]["build_ms"] = statistics.mean(build_ms)
+            # The probe is bound by random table lookups, not by HBM bytes: one
+            # 32-byte slot-pair read per probe. Its ceiling is the measured rate of
+            # random 32-B loads from an L2-resident table (tools/probe_ladder.cu
+            # rung 1: ~244 G/s, the L1TEX one-wavefront-per-clock limit); tables
+            # larger than L2 are capped by DRAM-random reads (~40 G/s measured).
+            # (the radix-partitioned path makes C4's lookups L2 lookups, so it is
+            # held to the L2 ceiling too).
+            table_in_l2 = table_bytes <= l2
+            partitioned = int(kt["join_slices"]) > 1
+            ceiling = LOOKUP_CEILING_L2 if (table_in_l2 or partitioned) else LOOKUP_CEILING_DRAM
+            lookups = len(pk) / (kms / 1e3) / 1e9
+            where = "L2-resident table" if table_in_l2 else ("table > L2, slice-partitioned" if partitioned
+                                                             else "table > L2")
+            line["roofline"]["lookup"] = {
+                "bound": f"random 32-B table lookups ({where})",
+                "achieved": lookups, "peak": ceiling, "unit": "Glookups/s", "frac": lookups / ceiling,
+                "peak_source": "tools/probe_ladder.cu, tools/microbench.cu (B200, this round)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+LOOKUP_CEILING_L2 = 244.0    # G random 32-B lookups/s, L2-resident table
+LOOKUP_CEILING_DRAM = 40.0   # G random 32-B lookups/s, table in HBM
 
 
 def main() -> None:
