@@ -114,6 +114,7 @@ struct Ctx {
   DevBuf sc_prow, sc_off, sc_cnt;
   DevBuf part_keys, part_pos, part_cnt, part_cur, run_base, run_len, res_part, work_ctr;
   DevBuf pairs_p, pairs_b;
+  DevBuf rows_flag;  // build row column is a dense run (join_build_impl)
   DevBuf srt_hist, srt_k0, srt_k1, srt_r0, srt_r1, srt_status, srt_base;
   DevBuf in_keys, in_rows, in_bkeys, in_brows, in_payload;
   uint64_t jcap = 0, jmask = 0, jnb = 0;
@@ -834,7 +835,13 @@ int probe_partitioned(const double* pkeys, uint64_t n, cudaStream_t s) {
   return GOLP_OK;
 }
 
-int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cudaStream_t s) {
+// rows_dense: 1 when the caller knows the build row column is a dense run (the
+// host regenerated it, upload_rows), 0 when unknown -- then a check kernel decides
+// on the device for columns beyond kDenseCheckMin entries (below that the gathers
+// hit L2 and the check would cost more than it saves).
+constexpr uint64_t kDenseCheckMin = 4u << 20;
+
+int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cudaStream_t s, int rows_dense = 0) {
   uint64_t cap = 1024;
   while (cap < 2 * nb && cap < (1ull << 32)) cap <<= 1;
   if (cap < 2 * nb || cap * kInline + nb > (1ull << 32)) {
@@ -854,6 +861,16 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   g.kt.join_capacity = cap;
   g.kt.join_slices = g.jparts;
   Slot* table = g.table.as<Slot>();
+  CK(g.rows_flag.ensure(4));
+  unsigned* dflag = g.rows_flag.as<unsigned>();
+  const bool check = !rows_dense && nb >= kDenseCheckMin;
+  CK(cudaMemsetAsync(dflag, (rows_dense || check) ? 1 : 0, 4, s));  // byte value 1 -> nonzero word
+  if (check) {
+    dense_rows_check_kernel<<<g.sms * 4, 256, 0, s>>>(brows, nb, dflag);
+    CKL();
+    ++g_launches;
+  }
+  const BuildRows br{brows, dflag};
   GroupArrays ga;
   ga.rows = g.rows_arr.as<uint32_t>();
   ga.ovf_slot = g.ovf.as<uint32_t>();
@@ -891,11 +908,11 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   else
     join_insert_kernel<false><<<gb, kBuildThreads, 0, s>>>(ikeys, ipos, nb, table, g.jmask, ga, sched);
   CKL();
-  join_finalize_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, brows, ga, cap * kInline);
+  join_finalize_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, br, ga, cap * kInline);
   CKL();
   join_overflow_kernel<<<g.sms, 256, 0, s>>>(table, ga);
   CKL();
-  join_group_sort_kernel<<<std::max(1, g.sms / 2), 128, 0, s>>>(table, ga, brows);
+  join_group_sort_kernel<<<std::max(1, g.sms / 2), 128, 0, s>>>(table, ga, br);
   CKL();
   static bool attr = false;
   const size_t smem = kGroupTile * sizeof(uint32_t);
@@ -903,7 +920,7 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
     CK(cudaFuncSetAttribute(join_big_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  join_big_groups_kernel<<<std::max(1, g.sms / 4), 1024, smem, s>>>(table, ga, brows);
+  join_big_groups_kernel<<<std::max(1, g.sms / 4), 1024, smem, s>>>(table, ga, br);
   CKL();
   g_launches += 5;
   prof_record(5, s);
@@ -1143,7 +1160,7 @@ int golp_shutdown(void) {
   DevBuf* bufs[] = {&g.ctl, &g.cand_hi, &g.cand_lo, &g.w_hi, &g.w_lo, &g.out_rows, &g.out_hi, &g.samples,
                     &g.table, &g.rows_arr, &g.ovf, &g.big_list, &g.jcount,
                     &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.srt_hist, &g.srt_k0, &g.srt_k1, &g.srt_r0, &g.srt_r1, &g.srt_status, &g.srt_base, &g.in_keys, &g.in_rows,
-                    &g.in_bkeys, &g.in_brows, &g.in_payload};
+                    &g.in_bkeys, &g.in_brows, &g.in_payload, &g.rows_flag};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < kSlots; ++i) {
     if (g.pin[i]) cudaFreeHost(g.pin[i]);
@@ -1543,13 +1560,14 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   RET(tr_mark());
   // build side first, then the probe side in chunks that are probed as they land
   RET(stage_h2d(dbk, build_keys, nb * 8));
-  RET(upload_rows(dbr, build_rows, nb));
+  bool brows_copied = true;
+  RET(upload_rows(dbr, build_rows, nb, &brows_copied));
   RET(tr_mark());
   if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(nb * (size_t)payload_bytes));
   cudaEvent_t ev_chunk = g.ev[0];
   CK(cudaEventRecord(ev_chunk, g.s_h2d));
   CK(cudaStreamWaitEvent(s, ev_chunk, 0));
-  RET(join_build_impl(dbk, dbr, nb, s));
+  RET(join_build_impl(dbk, dbr, nb, s, (nb > 0 && !brows_copied) ? 1 : 0));
 
   uint64_t per_chunk = std::max<uint64_t>(g.chunk / 8, kWarpTile);
   per_chunk = (per_chunk / kWarpTile) * kWarpTile;

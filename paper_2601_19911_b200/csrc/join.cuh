@@ -203,6 +203,39 @@ __global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double
   }
 }
 
+// Build position -> build row. When the row column is a dense run (*dense set by
+// dense_rows_check_kernel, or by the host when it regenerated the column),
+// rows[p] == rows[0] + p and the gather -- a random DRAM sector per entry once
+// the column outgrows L2 -- is skipped.
+struct BuildRows {
+  const uint32_t* rows;
+  const unsigned* dense;
+};
+struct RowMap {
+  const uint32_t* rows;
+  bool dense;
+  uint32_t base;
+  __device__ __forceinline__ explicit RowMap(const BuildRows& b)
+      : rows(b.rows), dense(*b.dense != 0), base(dense ? b.rows[0] : 0u) {}
+  __device__ __forceinline__ uint32_t operator()(uint32_t p) const { return dense ? base + p : __ldg(rows + p); }
+};
+
+// *flag (preset to 1) is cleared unless rows[i] == rows[0] + i for every i < n.
+__global__ void dense_rows_check_kernel(const uint32_t* __restrict__ rows, uint64_t n, unsigned* flag) {
+  const uint32_t b0 = rows[0];
+  bool bad = false;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t n4 = ((reinterpret_cast<uintptr_t>(rows) & 15) == 0) ? n / 4 : 0;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(rows) + q);
+    const uint32_t e = b0 + (uint32_t)(4 * q);
+    bad |= (v.x != e) | (v.y != e + 1u) | (v.z != e + 2u) | (v.w != e + 3u);
+  }
+  for (uint64_t i = 4 * n4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    bad |= rows[i] != b0 + (uint32_t)i;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 0u;
+}
+
 __device__ __forceinline__ void cswap_u32(uint32_t& a, uint32_t& b) {
   const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
   a = lo;
@@ -211,9 +244,10 @@ __device__ __forceinline__ void cswap_u32(uint32_t& a, uint32_t& b) {
 
 // One pass over the slots: singletons inline their row, groups of 2..kInline sort
 // their recorded positions and turn them into rows, big groups reserve a CSR range.
-__global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_t cap, const uint32_t* __restrict__ brows,
+__global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_t cap, BuildRows br,
                                                             GroupArrays ga, uint64_t csr_base) {
   const unsigned lane = lane_id();
+  const RowMap row(br);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t wb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; wb < cap; wb += stride) {
     const uint64_t h = wb + lane;
@@ -227,16 +261,16 @@ __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_
     }
     uint32_t* grp = ga.rows + h * kInline;
     if (cnt == 1) {
-      table[h].off = __ldg(brows + first);
+      table[h].off = row(first);
     } else if (cnt >= 2 && cnt <= kInline) {
       const uint4 v = *reinterpret_cast<const uint4*>(grp);
       uint32_t p0 = first, p1 = v.y, p2 = cnt > 2 ? v.z : 0xFFFFFFFFu, p3 = cnt > 3 ? v.w : 0xFFFFFFFFu;
       cswap_u32(p0, p1); cswap_u32(p2, p3); cswap_u32(p0, p2); cswap_u32(p1, p3); cswap_u32(p1, p2);
       uint4 o;
-      o.x = __ldg(brows + p0);
-      o.y = __ldg(brows + p1);
-      o.z = cnt > 2 ? __ldg(brows + p2) : 0u;
-      o.w = cnt > 3 ? __ldg(brows + p3) : 0u;
+      o.x = row(p0);
+      o.y = row(p1);
+      o.z = cnt > 2 ? row(p2) : 0u;
+      o.w = cnt > 3 ? row(p3) : 0u;
       *reinterpret_cast<uint4*>(grp) = o;
       table[h].off = (uint32_t)(h * kInline);
     }
@@ -275,8 +309,8 @@ __global__ void join_overflow_kernel(const Slot* __restrict__ table, GroupArrays
 // (insertion sort) and writes rows; larger ones are queued for the block kernel.
 constexpr uint32_t kThreadGroup = 32;
 
-__global__ void join_group_sort_kernel(const Slot* __restrict__ table, GroupArrays ga,
-                                       const uint32_t* __restrict__ brows) {
+__global__ void join_group_sort_kernel(const Slot* __restrict__ table, GroupArrays ga, BuildRows br) {
+  const RowMap row(br);
   const unsigned nbig = (unsigned)*(volatile unsigned long long*)&ga.counters[2];
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < nbig; gi += stride) {
@@ -294,7 +328,7 @@ __global__ void join_group_sort_kernel(const Slot* __restrict__ table, GroupArra
       while (q > 0 && p[q - 1] > v) { p[q] = p[q - 1]; --q; }
       p[q] = v;
     }
-    for (uint32_t m = 0; m < cnt; ++m) seg[m] = __ldg(brows + p[m]);
+    for (uint32_t m = 0; m < cnt; ++m) seg[m] = row(p[m]);
   }
 }
 
@@ -302,7 +336,8 @@ __global__ void join_group_sort_kernel(const Slot* __restrict__ table, GroupArra
 // group sorts its positions (shared memory up to kGroupTile, in place in global
 // memory beyond) and turns them into rows.
 __global__ void __launch_bounds__(1024) join_big_groups_kernel(const Slot* __restrict__ table, GroupArrays ga,
-                                                               const uint32_t* __restrict__ brows) {
+                                                               BuildRows br) {
+  const RowMap row(br);
   extern __shared__ __align__(16) uint32_t s_pos[];
   const unsigned nbig = (unsigned)*(volatile unsigned long long*)&ga.counters[2];
   const unsigned nhuge = (unsigned)*(volatile unsigned long long*)&ga.counters[3];
@@ -314,10 +349,10 @@ __global__ void __launch_bounds__(1024) join_big_groups_kernel(const Slot* __res
       for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) s_pos[m] = seg[m];
       __syncthreads();
       block_sort_asc_u32<false>(s_pos, cnt);
-      for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) seg[m] = __ldg(brows + s_pos[m]);
+      for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) seg[m] = row(s_pos[m]);
     } else {
       block_sort_asc_u32<true>(seg, cnt);
-      for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) seg[m] = __ldg(brows + __ldcg(seg + m));
+      for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) seg[m] = row(__ldcg(seg + m));
     }
     __syncthreads();
   }

@@ -240,3 +240,29 @@ def test_probe_keys_crowding_a_slice_boundary(b200, where):
     ep, eb = oracle.join(bk, br, pk, pr)
     assert res.payload.match_count == len(ep)
     assert np.array_equal(res.payload.probe_rows, ep) and np.array_equal(res.payload.build_rows, eb)
+
+
+@pytest.mark.parametrize("rows_kind", ["dense_offset", "one_swap", "permuted"])
+def test_join_build_row_column_density_check(cuda, rows_kind):
+    """Build sides of >= 4 Mi entries go through the on-device dense-row check:
+    a dense column lets the build skip the position -> row gathers, anything else
+    must keep them. Groups of every size class appear (domain = nb / 2)."""
+    import torch
+
+    from paper_2601_19911_b200 import resident
+
+    rng = np.random.default_rng(23)
+    nb, np_ = 5_000_000, 1_000_000
+    bk = rng.integers(0, nb // 2, size=nb).astype(np.float64)
+    pk = rng.integers(0, nb // 2, size=np_).astype(np.float64)
+    br = np.arange(nb, dtype=np.uint32) + 77
+    if rows_kind == "one_swap":
+        br[[nb - 3, nb - 2]] = br[[nb - 2, nb - 3]]
+    elif rows_kind == "permuted":
+        br = rng.permutation(br)
+    pr = np.arange(np_, dtype=np.uint32)
+    t = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(cuda)  # noqa: E731
+    op, ob = resident.join(t(bk), t(br), t(pk), t(pr))
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert np.array_equal(op.cpu().numpy().view(np.uint32), ep)
+    assert np.array_equal(ob.cpu().numpy().view(np.uint32), eb)
