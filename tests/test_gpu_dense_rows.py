@@ -127,3 +127,34 @@ def test_full_sort_dense_rows_same_answer(b200, copied):
         ref = copied.full_sort(KeyVector(keys, rows)).payload
         assert np.array_equal(got, ref)
         assert np.array_equal(got, rows[np.lexsort((rows, keys))])
+
+
+@pytest.mark.parametrize("bkind,pkind", [("arange", "permuted"), ("permuted", "arange"), ("arange", "arange")])
+def test_probe_mixed_density_and_full_row(b200, bkind, pkind):
+    """Dense and copied row columns on either side, key-only and full-row mode
+    (the full-row payload stream shares the copy queue with the key chunks)."""
+    from paper_2601_19911_b200 import FULL_ROW
+
+    rng = np.random.default_rng(41)
+    nb, np_ = 300_000, 4_500_000
+    bk = rng.integers(0, 2 * nb, size=nb).astype(np.float64)
+    pk = rng.integers(0, 2 * nb, size=np_).astype(np.float64)
+    mk = lambda kind, n: (np.arange(n, dtype=np.uint32) if kind == "arange"  # noqa: E731
+                          else rng.permutation(n).astype(np.uint32))
+    br, pr = mk(bkind, nb), mk(pkind, np_)
+    ep, eb = oracle.join(bk, br, pk, pr)
+    for mode, pb in (("key_only", None), (FULL_ROW, 20)):
+        res = b200.probe(KeyVector(bk, br), KeyVector(pk, pr), mode=mode, payload_bytes=pb)
+        assert np.array_equal(res.payload.probe_rows, ep) and np.array_equal(res.payload.build_rows, eb)
+
+
+@pytest.mark.parametrize("kind", ["arange", "one_chunk_permuted"])
+def test_topk_full_row_chunked_dense_rows(b200, kind):
+    from paper_2601_19911_b200 import FULL_ROW
+
+    rng = np.random.default_rng(43)
+    n = 5_000_000
+    keys = rng.integers(0, 1 << 53, size=n).astype(np.float64)
+    rows = _rows(kind, n, rng)
+    got = b200.topk(KeyVector(keys, rows), 500, mode=FULL_ROW, payload_bytes=12).payload.rows
+    assert np.array_equal(got, oracle.topk(keys, rows, 500))

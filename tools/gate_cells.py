@@ -1,0 +1,140 @@
+"""Config C5 (BASELINE.json) cell by cell on the B200: for every (op, N, K or M,
+mode) cell, P50/P95/P99 of end-to-end query latency (extract_keys + path +
+materialize, gate.execute_path semantics, pkg/src/golp/gate.py:167-233) for
+CPU-only (the host engine), always-on offload (B200Device) and the Risky Gate
+(execute_gated with the calibrated profile / CPU model), plus the gate's choice.
+
+    python tools/gate_cells.py [out.json] [--max-n N]
+
+The DeviceProfile is calibrated from B200 ledgers and the CpuCostModel from
+host-engine timings in the same run (tools/gate_sweep.py does the same); the
+gate then decides each cell with those constants. Repeats shrink with N so the
+whole sweep stays within a few minutes; percentiles are nearest-rank
+(pkg/src/golp/harness.py:127-143)."""
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+from paper_2601_19911_b200 import (  # noqa: E402
+    B200Device, FULL_ROW, KEY_ONLY, OP_PROBE, OP_TOPK, GateConfig, calibrate_cpu_model, host_topk,
+    random_key_vector)
+from paper_2601_19911_b200.gate import DEVICE, HOST, execute_gated, execute_path  # noqa: E402
+from paper_2601_19911_b200.harness import calibrate_device_profile, compute_stats, table_seed  # noqa: E402
+from paper_2601_19911_b200.host import host_hash_build, host_hash_probe  # noqa: E402
+from paper_2601_19911_b200.store import ColumnTable, extract_keys, generate_table  # noqa: E402
+
+
+def repeats_for(n):
+    return 25 if n <= 100_000 else (11 if n <= 1_000_000 else (5 if n <= 10_000_000 else 3))
+
+
+def stats(ts):
+    s = compute_stats(ts)
+    return {"p50": s.median, "p95": s.p95, "p99": s.p99}
+
+
+def probe_tables(n, payload, seed):
+    """Probe side of n rows, build side n/10 rows, keys uniform in [0, 2 * build):
+    ~0.5 matches per probe (BASELINE's join shape)."""
+    nb = max(1, n // 10)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    bk = rng.integers(0, 2 * nb, nb).astype(np.float64)
+    pk = rng.integers(0, 2 * nb, n).astype(np.float64)
+    pay = lambda m: np.zeros((m, payload), dtype=np.uint8)  # noqa: E731
+    return ColumnTable(bk, pay(nb), seed), ColumnTable(pk, pay(n), seed + 1)
+
+
+def run_cell(tables, op, k, cfg, dev, reps):
+    """Warm each path twice (B200Device page-locks a reused input column on its
+    second call, a one-off ~0.1-0.4 s at 1e8 rows that a query stream amortizes),
+    then interleave host / device / gated per repeat."""
+    for _ in range(2):
+        for path in (HOST, DEVICE):
+            execute_path(tables, op, k, cfg, dev, path)
+    host, devt, gated = [], [], []
+    choice = None
+    for _ in range(reps):
+        host.append(execute_path(tables, op, k, cfg, dev, HOST)[1])
+        devt.append(execute_path(tables, op, k, cfg, dev, DEVICE)[1])
+        _, decision, t = execute_gated(tables, op, k, cfg, dev)
+        gated.append(t)
+        choice = decision.path
+    return {"cpu_only": stats(host), "always_on": stats(devt), "gated": stats(gated), "gate_choice": choice,
+            "repeats": reps}
+
+
+def main(out_path, max_n):
+    t0 = time.time()
+    dev = B200Device()
+    prof = calibrate_device_profile(dev, ns=(100_000, 1_000_000, 4_000_000, 16_000_000), repeats=3,
+                                    probe_ns=(200_000, 2_000_000, 8_000_000))
+    samples = []
+    for n in (100_000, 1_000_000, 4_000_000, 16_000_000):  # host Top-K (sort family)
+        kv = random_key_vector(n, n)
+        host_topk(kv, 100)
+        samples.append((OP_TOPK, n, 100, _time(lambda: host_topk(kv, 100))))
+    # host probe (match family). The reference's form is alpha_match * n * k + beta
+    # (pkg/src/golp/gate.py:37-160); a hash join's host cost grows with n alone, so
+    # the samples pass k = 1 and alpha_match comes out per probe. Cells with M = 1
+    # are then the well-posed gate; cells with M = expected matches show what the
+    # n * M form does with that constant.
+    for n in (100_000, 1_000_000, 4_000_000):
+        b, p = probe_tables(n, 1, n)
+        bkv, pkv = extract_keys(b), extract_keys(p)
+        samples.append((OP_PROBE, n, 1, _time(lambda: host_hash_probe(host_hash_build(bkv), pkv))))
+    cpu = calibrate_cpu_model(samples)
+    cells = []
+    ns = [n for n in (1_000, 10_000, 100_000, 1_000_000, 10_000_000, 100_000_000) if n <= max_n]
+    for n in ns:
+        for mode in (KEY_ONLY, FULL_ROW):
+            if mode == FULL_ROW and n > 10_000_000:
+                continue  # 196 B/row: 19.6 GB per call at 1e8 -- host RAM, not the device, is the limit
+            payload = 188 if mode == FULL_ROW else 1  # key-only never ships the payload
+            cfg = GateConfig(mode=mode, profile=prof, cpu_model=cpu)
+            table = generate_table(n, payload_bytes=payload, seed=table_seed(7, n),
+                                   memory_budget=1 << 40)
+            for k in (10, 1000, 100_000):
+                if k > n:
+                    continue
+                cell = {"op": OP_TOPK, "n": n, "k": k, "mode": mode}
+                cell.update(run_cell(table, OP_TOPK, k, cfg, dev, repeats_for(n)))
+                cells.append(cell)
+                print(json.dumps(cell), flush=True)
+            del table
+            tables = probe_tables(n, payload, table_seed(9, n))
+            for m in (1, n // 2):  # the gate's M: a point estimate and the expected match count
+                cell = {"op": OP_PROBE, "n": n, "build_n": tables[0].row_count, "m": m, "mode": mode}
+                cell.update(run_cell(tables, OP_PROBE, max(m, 1), cfg, dev, repeats_for(n)))
+                cells.append(cell)
+                print(json.dumps(cell), flush=True)
+    # per cell, how the gate's percentiles compare with the better fixed strategy
+    for c in cells:
+        for q in ("p95", "p99"):
+            best = min(c["cpu_only"][q], c["always_on"][q])
+            c[f"gated_{q}_over_best_fixed"] = c["gated"][q] / best if best > 0 else None
+    out = {"profile_b200": prof.to_json_dict(), "cpu_model_host_engine": cpu.to_json_dict(), "cells": cells,
+           "wall_s": time.time() - t0}
+    Path(out_path).write_text(json.dumps(out, indent=1))
+    dev.close()
+
+
+def _time(fn, reps=3):
+    ts = []
+    for _ in range(reps):
+        a = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - a)
+    return sorted(ts)[len(ts) // 2]
+
+
+if __name__ == "__main__":
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    max_n = 100_000_000
+    if "--max-n" in sys.argv:
+        max_n = int(float(sys.argv[sys.argv.index("--max-n") + 1]))
+    main(args[0] if args else "gpurun_out/gate_cells.json", max_n)
