@@ -903,7 +903,10 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
     CK(cudaMemsetAsync(g.work_ctr.p, 0, 8, s));
     sched.ctr = g.work_ctr.as<unsigned long long>();
   }
-  if (g.jparts > 1)  // table in HBM: one 16-byte CAS per new key
+#ifndef GOLP_BUILD_WIDE_ALWAYS
+#define GOLP_BUILD_WIDE_ALWAYS 0
+#endif
+  if (g.jparts > 1 || GOLP_BUILD_WIDE_ALWAYS)  // table in HBM: one 16-byte CAS per new key
     join_insert_kernel<true><<<gb, kBuildThreads, 0, s>>>(ikeys, ipos, nb, table, g.jmask, ga, sched);
   else
     join_insert_kernel<false><<<gb, kBuildThreads, 0, s>>>(ikeys, ipos, nb, table, g.jmask, ga, sched);
@@ -912,7 +915,7 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   CKL();
   join_overflow_kernel<<<g.sms, 256, 0, s>>>(table, ga);
   CKL();
-  join_group_sort_kernel<<<std::max(1, g.sms / 2), 128, 0, s>>>(table, ga, br);
+  join_group_sort_kernel<<<g.sms, 256, 0, s>>>(table, ga, br);
   CKL();
   static bool attr = false;
   const size_t smem = kGroupTile * sizeof(uint32_t);

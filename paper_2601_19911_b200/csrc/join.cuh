@@ -82,8 +82,14 @@ __global__ void join_init_table_kernel(Slot* __restrict__ table, uint64_t cap) {
 // Build kernels process tiles of kBuildThreads*kBuildItems consecutive entries;
 // each thread owns kBuildItems entries strided by the block size (coalesced),
 // and issues their loads / atomics together so the dependent chains overlap.
-constexpr int kBuildThreads = 256;
-constexpr int kBuildItems = 4;
+#ifndef GOLP_BUILD_THREADS
+#define GOLP_BUILD_THREADS 512
+#endif
+#ifndef GOLP_BUILD_ITEMS
+#define GOLP_BUILD_ITEMS 1
+#endif
+constexpr int kBuildThreads = GOLP_BUILD_THREADS;
+constexpr int kBuildItems = GOLP_BUILD_ITEMS;
 constexpr uint64_t kBuildTile = (uint64_t)kBuildThreads * kBuildItems;
 
 struct GroupArrays {
@@ -310,25 +316,30 @@ __global__ void join_overflow_kernel(const Slot* __restrict__ table, GroupArrays
 constexpr uint32_t kThreadGroup = 32;
 
 __global__ void join_group_sort_kernel(const Slot* __restrict__ table, GroupArrays ga, BuildRows br) {
+  // one warp per group: lane m holds member m's position, its rank among the
+  // group's (distinct) positions is its place in build order
   const RowMap row(br);
+  const unsigned lane = lane_id();
   const unsigned nbig = (unsigned)*(volatile unsigned long long*)&ga.counters[2];
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < nbig; gi += stride) {
+  const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t gi = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gi < nbig; gi += wstride) {
     const uint32_t h = ga.big_list[gi];
     const uint32_t cnt = table[h].cnt;
     if (cnt > kThreadGroup) {
-      ga.big_list[nbig + atomicAdd(&ga.counters[3], 1ull)] = h;  // block kernel's queue
+      if (lane == 0) ga.big_list[nbig + atomicAdd(&ga.counters[3], 1ull)] = h;  // block kernel's queue
       continue;
     }
     uint32_t* seg = ga.rows + table[h].off;
-    uint32_t p[kThreadGroup];
-    for (uint32_t m = 0; m < cnt; ++m) {
-      const uint32_t v = seg[m];
-      uint32_t q = m;
-      while (q > 0 && p[q - 1] > v) { p[q] = p[q - 1]; --q; }
-      p[q] = v;
+    const uint32_t v = lane < cnt ? seg[lane] : 0xFFFFFFFFu;
+    uint32_t rank = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t u = __shfl_sync(0xFFFFFFFFu, v, j);
+      rank += (u < v) || (u == v && j < (int)lane);
     }
-    for (uint32_t m = 0; m < cnt; ++m) seg[m] = row(p[m]);
+    const uint32_t r = lane < cnt ? row(v) : 0u;
+    __syncwarp();
+    if (lane < cnt) seg[rank] = r;
   }
 }
 
