@@ -28,6 +28,12 @@ namespace golp {
 #ifndef GOLP_SORT_MINB
 #define GOLP_SORT_MINB 4
 #endif
+#ifndef GOLP_SORT_LOOK_WINDOW
+#define GOLP_SORT_LOOK_WINDOW 4
+#endif
+#ifndef GOLP_SORT_SPIN_NS
+#define GOLP_SORT_SPIN_NS 0
+#endif
 constexpr int kSortThreads = GOLP_SORT_THREADS;
 constexpr int kSortItems = GOLP_SORT_ITEMS;
 constexpr uint32_t kSortTileN = (uint32_t)kSortThreads * kSortItems;  // 2048 items
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(kSortThreads, GOLP_SORT_MINB) sort_pass_kernel
     const int d = threadIdx.x;
     unsigned long long excl = 0;
     if (tile > 0) {
-      constexpr int kLookWindow = 8;
+      constexpr int kLookWindow = GOLP_SORT_LOOK_WINDOW;
       int64_t p = (int64_t)tile - 1;
       bool done = false;
       while (!done && p >= 0) {
@@ -198,8 +204,10 @@ __global__ void __launch_bounds__(kSortThreads, GOLP_SORT_MINB) sort_pass_kernel
 #pragma unroll
         for (int u = 0; u < kLookWindow; ++u) {
           if (done || p - u < 0) continue;
-          while ((v[u] & ~kStatValue) == 0)
+          while ((v[u] & ~kStatValue) == 0) {
+            if (GOLP_SORT_SPIN_NS) __nanosleep(GOLP_SORT_SPIN_NS);
             v[u] = *(const volatile unsigned long long*)(a.status + (uint64_t)(p - u) * 256 + d);
+          }
           excl += v[u] & kStatValue;
           if (v[u] & kStatPrefix) done = true;
         }
