@@ -1015,11 +1015,21 @@ __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch s
           st_hint(out_b + g, of[q], pol_stream);
         }
       } else {
-        for (uint32_t m = 0; m < c[q]; ++m, ++g)
-          if (g < cap) {
-            st_hint(out_p + g, pr[q], pol_stream);
-            st_hint(out_b + g, __ldg(csr_row + of[q] + m), pol_stream);
+        // a key group: its rows are contiguous (CSR / side array); four
+        // independent loads per step instead of one dependent load per member
+        for (uint32_t m0 = 0; m0 < c[q]; m0 += 4) {
+          uint32_t br[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) br[u] = m0 + u < c[q] ? __ldg(csr_row + of[q] + m0 + u) : 0u;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned long long gg = g + m0 + u;
+            if (m0 + u < c[q] && gg < cap) {
+              st_hint(out_p + gg, pr[q], pol_stream);
+              st_hint(out_b + gg, br[u], pol_stream);
+            }
           }
+        }
       }
       run += __shfl_sync(0xFFFFFFFFu, incl, 31);
     }
