@@ -17,4 +17,5 @@ run c3_k10 --workload topk_c3 --k 10
 run c3_k1000 --workload topk_c3 --k 1000
 run c3_k100000 --workload topk_c3 --k 100000
 run c3_zipfhi --workload topk_c3 --k 1000 --dist zipf_hi --no-cpu-baseline
+run c3_zipflo --workload topk_c3 --k 1000 --dist zipf_lo --no-cpu-baseline
 run c4 --workload join_c4
