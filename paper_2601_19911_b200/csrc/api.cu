@@ -805,12 +805,12 @@ int partition_entries(const double* keys, uint64_t n, bool probe_side, cudaStrea
   CKL();
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(part_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartSmem));
+    CK(cudaFuncSetAttribute(part_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartScatterSmem));
     attr = true;
   }
-  static const int gsmax = resident_grid(part_scatter_kernel, kPartThreads, kPartSmem);
+  static const int gsmax = resident_grid(part_scatter_kernel, kPartThreads, kPartScatterSmem);
   const int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)gsmax));
-  part_scatter_kernel<<<gs, kPartThreads, kPartSmem, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cur, o);
+  part_scatter_kernel<<<gs, kPartThreads, kPartScatterSmem, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cur, o);
   CKL();
   g_launches += 3;
   return GOLP_OK;

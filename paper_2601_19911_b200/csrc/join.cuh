@@ -493,6 +493,37 @@ static_assert(kPartItems * kPartThreads == (int)kPartTile && kPartItems % 2 == 0
 constexpr uint32_t kMaxParts = 1024;
 constexpr uint32_t kMaxProbeParts = 256;  // bounds the per-(tile, slice) run table
 constexpr size_t kPartSmem = (size_t)kPartTile * (8 + 2 + 2) + (size_t)kMaxParts * (4 + 4 + 8);
+#ifndef GOLP_PART_TMA
+#define GOLP_PART_TMA 1
+#endif
+// + the next tile's keys, prefetched by TMA while the current tile is processed
+constexpr size_t kPartScatterSmem = kPartSmem + (GOLP_PART_TMA ? (size_t)kPartTile * 8 : 0);
+
+// ---- TMA bulk copies (cp.async.bulk, mbarrier completion) ----------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+// One thread: expect `bytes` on the barrier, then a bulk global -> shared copy
+// that completes them (16-byte aligned addresses, size a multiple of 16).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar, uint64_t pol) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst), b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(b),
+      "r"(phase)
+      : "memory");
+}
 
 __device__ __forceinline__ uint32_t part_of(double k, uint32_t mask, int slice_bits) {
   return home_slot32(canon_bits(k), mask) >> slice_bits;
@@ -578,14 +609,43 @@ __global__ void __launch_bounds__(kPartThreads, GOLP_PART_MINB) part_scatter_ker
   __shared__ unsigned long long s_w[33];
   const uint64_t pol = policy_evict_first();
   const uint64_t ntiles = (n + kPartTile - 1) / kPartTile;
+  // Full tiles of a 16-byte aligned key column arrive by TMA: one thread
+  // issues the next tile's 32 KB bulk copy as soon as the block has read the
+  // current one, so the load overlaps the ranking, scan and scatter.
+  double* s_in = reinterpret_cast<double*>(smem + kPartSmem);
+  __shared__ __align__(8) uint64_t s_bar;
+  const bool tma = GOLP_PART_TMA && (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
+  auto tma_tile = [&](uint64_t t) { return tma && t < ntiles && (t + 1) * kPartTile <= n; };
+  unsigned phase = 0;
+  if (tma) {
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar, 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && tma_tile(blockIdx.x))
+      bulk_g2s(s_in, keys + (uint64_t)blockIdx.x * kPartTile, kPartTile * 8, &s_bar, pol);
+  }
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const uint64_t t0 = t * kPartTile;
     const uint32_t cnt = (uint32_t)(n - t0 < kPartTile ? n - t0 : kPartTile);
     for (uint32_t p = threadIdx.x; p < nparts; p += blockDim.x) s_cnt[p] = 0;
-    __syncthreads();
     double k[kPartItems];
     uint32_t pr[kPartItems];  // part << 16 | rank inside the tile's run
-    if (cnt == kPartTile && ((reinterpret_cast<uintptr_t>(keys + t0) & 15) == 0)) {
+    if (tma_tile(t)) {
+      mbar_wait(&s_bar, phase);
+      phase ^= 1u;
+#pragma unroll
+      for (int j = 0; j < kPartItems; j += 2) {
+        const double2 v = reinterpret_cast<const double2*>(s_in)[threadIdx.x + (j >> 1) * kPartThreads];
+        k[j] = v.x;
+        k[j + 1] = v.y;
+      }
+      __syncthreads();  // s_in consumed (and s_cnt cleared) before the next copy lands in it
+      if (threadIdx.x == 0 && tma_tile(t + gridDim.x))
+        bulk_g2s(s_in, keys + (t + gridDim.x) * kPartTile, kPartTile * 8, &s_bar, pol);
+    } else if (cnt == kPartTile && ((reinterpret_cast<uintptr_t>(keys + t0) & 15) == 0)) {
+      __syncthreads();
 #pragma unroll
       for (int j = 0; j < kPartItems; j += 2) {
         const double2 v = ldg_stream_d2(keys + t0 + 2 * threadIdx.x + (uint64_t)j * kPartThreads, pol);
@@ -593,6 +653,7 @@ __global__ void __launch_bounds__(kPartThreads, GOLP_PART_MINB) part_scatter_ker
         k[j + 1] = v.y;
       }
     } else {
+      __syncthreads();
 #pragma unroll
       for (int j = 0; j < kPartItems; j += 2) {
         const uint32_t l = 2 * threadIdx.x + j * kPartThreads;
