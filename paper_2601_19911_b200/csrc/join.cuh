@@ -536,6 +536,12 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(const double* 
   for (uint32_t p = threadIdx.x; p < nparts; p += blockDim.x) s_h[p] = 0;
   __syncthreads();
   const uint64_t pol = policy_evict_first();
+  // 16-byte pair loads from the first 16-byte boundary on; a column that starts
+  // 8 bytes off it (a view) counts its first key on its own
+  const uint64_t head = (n > 0 && (reinterpret_cast<uintptr_t>(keys) & 15) != 0) ? 1 : 0;
+  if (head && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&s_h[part_of(keys[0], mask, slice_bits)], 1u);
+  keys += head;
+  n -= head;
   const uint64_t n2 = n / 2;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -266,3 +266,49 @@ def test_join_build_row_column_density_check(cuda, rows_kind):
     ep, eb = oracle.join(bk, br, pk, pr)
     assert np.array_equal(op.cpu().numpy().view(np.uint32), ep)
     assert np.array_equal(ob.cpu().numpy().view(np.uint32), eb)
+
+
+@pytest.mark.parametrize("offset", [1, 2])
+def test_partitioned_join_misaligned_key_columns(cuda, monkeypatch, offset):
+    """Key columns that start 8 bytes off a 16-byte boundary (tensor views) take
+    the partition scatter's plain-load path instead of the TMA bulk copies; both
+    sides, every tile, same answer."""
+    import torch
+
+    from paper_2601_19911_b200 import resident
+
+    monkeypatch.setenv("GOLP_JOIN_SLICE_BYTES", "65536")
+    monkeypatch.setenv("GOLP_JOIN_PART_PROBE", "1")
+    rng = np.random.default_rng(31 + offset)
+    nb, np_ = 300_000, 1_000_000
+    bk = rng.integers(0, 600_000, size=nb + offset).astype(np.float64)
+    pk = rng.integers(0, 600_000, size=np_ + offset).astype(np.float64)
+    br = rng.permutation(nb).astype(np.uint32)
+    pr = rng.permutation(np_).astype(np.uint32)
+    t = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(cuda)  # noqa: E731
+    tbk, tpk = t(bk)[offset:], t(pk)[offset:]
+    assert (tbk.data_ptr() % 16 != 0) == (offset % 2 == 1)
+    op, ob = resident.join(tbk, t(br), tpk, t(pr))
+    ep, eb = oracle.join(bk[offset:], br, pk[offset:], pr)
+    assert np.array_equal(op.cpu().numpy().view(np.uint32), ep)
+    assert np.array_equal(ob.cpu().numpy().view(np.uint32), eb)
+
+
+def test_resident_topk_and_sort_misaligned_views(cuda):
+    """Top-K and the full sort over key / row views that start off a 16-byte
+    boundary (vector loads must not assume the allocation's alignment)."""
+    import torch
+
+    from paper_2601_19911_b200 import resident
+
+    rng = np.random.default_rng(37)
+    n = 3_000_001
+    keys = rng.integers(0, 1 << 40, size=n + 1).astype(np.float64)
+    rows = rng.permutation(n + 1).astype(np.uint32)
+    tk = torch.from_numpy(keys).to(cuda)[1:]
+    tr = torch.from_numpy(rows.view(np.int32)).to(cuda)[1:]
+    got = resident.topk(tk, tr, 777)
+    got = (got[0] if isinstance(got, tuple) else got).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, oracle.topk(keys[1:], rows[1:], 777))
+    srt = resident.full_sort(tk, tr).cpu().numpy().view(np.uint32)
+    assert np.array_equal(srt, rows[1:][np.lexsort((rows[1:], keys[1:]))])
