@@ -1521,6 +1521,9 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
   return GOLP_OK;
 }
 
+#ifndef GOLP_TAIL_SPLIT
+#define GOLP_TAIL_SPLIT 4
+#endif
 int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb, const double* probe_keys,
                const uint32_t* probe_rows, uint64_t np, int mode, uint32_t payload_bytes, uint32_t* out_probe_rows,
                uint32_t* out_build_rows, uint64_t out_cap, uint64_t* out_matches, golp_ledger* led) {
@@ -1577,7 +1580,7 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   // Chunk bounds: full staging chunks, then the last chunk's worth of probes in
   // kTailSplit pieces, so the work left after the final upload (its probe and
   // its pairs' download) is a fraction of a chunk.
-  constexpr uint64_t kTailSplit = 4;
+  constexpr uint64_t kTailSplit = GOLP_TAIL_SPLIT;
   std::vector<uint64_t> cb{0};
   while (cb.back() < np) {
     const uint64_t left = np - cb.back();
