@@ -158,3 +158,22 @@ def test_topk_full_row_chunked_dense_rows(b200, kind):
     rows = _rows(kind, n, rng)
     got = b200.topk(KeyVector(keys, rows), 500, mode=FULL_ROW, payload_bytes=12).payload.rows
     assert np.array_equal(got, oracle.topk(keys, rows, 500))
+
+
+@pytest.mark.parametrize("n", [CHUNK - 1, CHUNK, CHUNK + 1, 2 * CHUNK + 1, 2 * CHUNK + 63])
+def test_chunk_boundaries_dense_rows(b200, n):
+    """Inputs one entry either side of the staging-chunk size: single-entry tail
+    chunks are dense runs by definition and must be filled, not skipped."""
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, 1 << 53, size=n).astype(np.float64)
+    rows = np.arange(n, dtype=np.uint32) + 5
+    keys[-1] = float(1 << 53)  # the last entry is the maximum: it must come back first
+    got = b200.topk(KeyVector(keys, rows), 50).payload.rows
+    assert got[0] == rows[-1]
+    assert np.array_equal(got, oracle.topk(keys, rows, 50))
+    bk = rng.integers(0, 1000, size=3000).astype(np.float64)
+    pk = rng.integers(0, 1000, size=n).astype(np.float64)
+    pr = rows
+    res = b200.probe(KeyVector(bk, np.arange(3000, dtype=np.uint32)), KeyVector(pk, pr)).payload
+    ep, eb = oracle.join(bk, np.arange(3000, dtype=np.uint32), pk, pr)
+    assert np.array_equal(res.probe_rows, ep) and np.array_equal(res.build_rows, eb)
