@@ -115,6 +115,7 @@ struct Ctx {
   DevBuf part_keys, part_pos, part_cnt, part_cur, run_base, run_len, res_part, work_ctr;
   DevBuf pairs_p, pairs_b;
   DevBuf rows_flag;  // build row column is a dense run (join_build_impl)
+  DevBuf row_base;   // what the emit adds to a singleton's slot.off (rows[0] for a dense column, else 0)
   DevBuf srt_hist, srt_k0, srt_k1, srt_r0, srt_r1, srt_status, srt_base;
   DevBuf in_keys, in_rows, in_bkeys, in_brows, in_payload;
   uint64_t jcap = 0, jmask = 0, jnb = 0;
@@ -837,9 +838,10 @@ int probe_partitioned(const double* pkeys, uint64_t n, cudaStream_t s) {
 
 // rows_dense: 1 when the caller knows the build row column is a dense run (the
 // host regenerated it, upload_rows), 0 when unknown -- then a check kernel decides
-// on the device for columns beyond kDenseCheckMin entries (below that the gathers
-// hit L2 and the check would cost more than it saves).
-constexpr uint64_t kDenseCheckMin = 4u << 20;
+// on the device for columns beyond kDenseCheckMin entries (below that the check
+// would cost more than it saves). With a dense column singletons keep their
+// position (the emit adds rows[0]): the finalize neither gathers nor stores them.
+constexpr uint64_t kDenseCheckMin = 256u << 10;
 
 int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cudaStream_t s, int rows_dense = 0) {
   uint64_t cap = 1024;
@@ -854,6 +856,7 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   CK(g.ovf.ensure(nbb * 12));
   CK(g.big_list.ensure((nbb / (kInline + 1) * 2 + 2) * 4));
   CK(g.jcount.ensure(32));
+  CK(g.row_base.ensure(4));
   g.jcap = cap;
   g.jmask = cap - 1;
   g.jnb = nb;
@@ -911,7 +914,8 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   else
     join_insert_kernel<false><<<gb, kBuildThreads, 0, s>>>(ikeys, ipos, nb, table, g.jmask, ga, sched);
   CKL();
-  join_finalize_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, br, ga, cap * kInline);
+  join_finalize_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, br, ga, cap * kInline,
+                                                               g.row_base.as<uint32_t>());
   CKL();
   join_overflow_kernel<<<g.sms, 256, 0, s>>>(table, ga);
   CKL();
@@ -1000,13 +1004,15 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
       ++ci;
       if (blocks <= kInlineScanBlocks) {  // emit blocks add up the earlier blocks' totals themselves
         join_emit_kernel<false><<<(unsigned)blocks, kProbeThreads, 0, s>>>(
-            sc, g.rows_arr.as<uint32_t>(), nwt, per_warp, part, bin, bout, out_p, out_b, cap);
+            sc, g.rows_arr.as<uint32_t>(), nwt, per_warp, part, bin, bout, out_p, out_b, cap,
+            g.row_base.as<uint32_t>());
       } else {
         scan_partials_kernel<<<1, kScanThreads, 0, s>>>(part, (uint32_t)blocks, bin, bout);
         CKL();
         ++g_launches;
         join_emit_kernel<true><<<(unsigned)blocks, kProbeThreads, 0, s>>>(
-            sc, g.rows_arr.as<uint32_t>(), nwt, per_warp, part, bin, bout, out_p, out_b, cap);
+            sc, g.rows_arr.as<uint32_t>(), nwt, per_warp, part, bin, bout, out_p, out_b, cap,
+            g.row_base.as<uint32_t>());
       }
       CKL();
       g_launches += 2;
@@ -1163,7 +1169,7 @@ int golp_shutdown(void) {
   DevBuf* bufs[] = {&g.ctl, &g.cand_hi, &g.cand_lo, &g.w_hi, &g.w_lo, &g.out_rows, &g.out_hi, &g.samples,
                     &g.table, &g.rows_arr, &g.ovf, &g.big_list, &g.jcount,
                     &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.srt_hist, &g.srt_k0, &g.srt_k1, &g.srt_r0, &g.srt_r1, &g.srt_status, &g.srt_base, &g.in_keys, &g.in_rows,
-                    &g.in_bkeys, &g.in_brows, &g.in_payload, &g.rows_flag};
+                    &g.in_bkeys, &g.in_brows, &g.in_payload, &g.rows_flag, &g.row_base};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < kSlots; ++i) {
     if (g.pin[i]) cudaFreeHost(g.pin[i]);

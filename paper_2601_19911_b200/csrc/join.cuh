@@ -250,10 +250,13 @@ __device__ __forceinline__ void cswap_u32(uint32_t& a, uint32_t& b) {
 
 // One pass over the slots: singletons inline their row, groups of 2..kInline sort
 // their recorded positions and turn them into rows, big groups reserve a CSR range.
+// Dense row column: singletons keep their build POSITION in slot.off (the emit
+// adds the column's first row id, *row_base): no gather and no store for them.
 __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_t cap, BuildRows br,
-                                                            GroupArrays ga, uint64_t csr_base) {
+                                                            GroupArrays ga, uint64_t csr_base, uint32_t* row_base) {
   const unsigned lane = lane_id();
   const RowMap row(br);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *row_base = row.dense ? row.base : 0u;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t wb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; wb < cap; wb += stride) {
     const uint64_t h = wb + lane;
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_
     }
     uint32_t* grp = ga.rows + h * kInline;
     if (cnt == 1) {
-      table[h].off = row(first);
+      if (!row.dense) table[h].off = row(first);
     } else if (cnt >= 2 && cnt <= kInline) {
       const uint4 v = *reinterpret_cast<const uint4*>(grp);
       uint32_t p0 = first, p1 = v.y, p2 = cnt > 2 ? v.z : 0xFFFFFFFFu, p3 = cnt > 3 ? v.w : 0xFFFFFFFFu;
@@ -1024,7 +1027,8 @@ __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch s
                                                                   const unsigned long long* __restrict__ base_in,
                                                                   unsigned long long* __restrict__ total_out,
                                                                   uint32_t* __restrict__ out_p,
-                                                                  uint32_t* __restrict__ out_b, uint64_t cap) {
+                                                                  uint32_t* __restrict__ out_b, uint64_t cap,
+                                                                  const uint32_t* __restrict__ row_base) {
   __shared__ unsigned long long s_wp[kProbeWarps];
   __shared__ unsigned long long s_red[kProbeWarps];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -1050,6 +1054,7 @@ __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch s
   for (unsigned w = 0; w < warp; ++w) run += s_wp[w];
   if (lo >= nwt) return;
   const uint64_t pol_stream = policy_evict_first();
+  const uint32_t rb = __ldg(row_base);
   const uint64_t e0 = lo * kWarpTile;
   const uint32_t ne = sc.wentries[gw];
   constexpr int kBatch = 4;  // 4 x 32 entries in flight per warp iteration
@@ -1076,10 +1081,10 @@ __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch s
         if ((int)lane >= o) incl += v;
       }
       unsigned long long g = run + (incl - c[q]);
-      if (c[q] == 1) {
+      if (c[q] == 1) {  // singleton: slot.off is its row, or its position past the first row id
         if (g < cap) {
           st_hint(out_p + g, pr[q], pol_stream);
-          st_hint(out_b + g, of[q], pol_stream);
+          st_hint(out_b + g, of[q] + rb, pol_stream);
         }
       } else {
         // a key group: its rows are contiguous (CSR / side array); four
