@@ -685,6 +685,8 @@ int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint6
           set_error("topk_fused_kernel cannot be co-resident");
           return GOLP_ERR_CUDA;
         }
+        // blocks per SM (test / tuning knob GOLP_TOPK_FUSED_PER_SM; default: all that fit)
+        per = (int)std::min<uint64_t>((uint64_t)per, std::max<uint64_t>(1, env_u64("GOLP_TOPK_FUSED_PER_SM", per)));
         blocks = per * g.sms;
       }
       void* args[] = {&f};
