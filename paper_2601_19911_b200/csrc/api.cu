@@ -689,6 +689,7 @@ int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint6
         per = (int)std::min<uint64_t>((uint64_t)per, std::max<uint64_t>(1, env_u64("GOLP_TOPK_FUSED_PER_SM", per)));
         blocks = per * g.sms;
       }
+      CK(cudaMemsetAsync(ctl(1), 0, 2 * sizeof(SelectCtl), s));  // candidate + fallback controls
       void* args[] = {&f};
       CK(cudaLaunchCooperativeKernel((void*)topk_fused_kernel, blocks, kSelThreads, args, smem, s));
       ++g_launches;

@@ -519,6 +519,93 @@ constexpr size_t kRankSmem = (size_t)kRankMax * (sizeof(uint64_t) + sizeof(uint3
 
 // Exact ranks of the m items staged in shared memory, computed for a strided
 // share of the items by every warp of the grid (see above).
+// Block-local MSB radix select over m staged items (96-bit composite, 8-bit
+// digits): the largest prefix P (low bits zero) such that exactly `need` items
+// are >= P. Every block computes the same P from the same items, so the fused
+// Top-K needs no grid barrier to publish its threshold. Called by all threads.
+__device__ __forceinline__ void block_radix_threshold(const uint64_t* s_hi, const uint32_t* s_lo, uint32_t m,
+                                                      uint64_t need, uint64_t* out_hi, uint32_t* out_lo) {
+  __shared__ unsigned s_h[256];
+  __shared__ uint64_t sh_hi;
+  __shared__ uint32_t sh_lo;
+  __shared__ int sh_bits, sh_done;
+  __shared__ unsigned long long sh_rem;
+  uint64_t pre_hi = 0;
+  uint32_t pre_lo = 0;
+  int bits = 0;
+  unsigned long long rem = need;
+  for (int pass = 0; pass < 12; ++pass) {
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) s_h[t] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const uint64_t h = s_hi[i];
+      unsigned d;
+      if (bits < 64) {
+        if (bits > 0 && (h >> (64 - bits)) != (pre_hi >> (64 - bits))) continue;
+        d = (unsigned)(h >> (56 - bits)) & 255u;
+      } else {
+        if (h != pre_hi) continue;
+        const uint32_t l = s_lo[i];
+        if (bits > 64 && (l >> (96 - bits)) != (pre_lo >> (96 - bits))) continue;
+        d = (l >> (24 - (bits - 64))) & 255u;
+      }
+      atomicAdd(&s_h[d], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // lane covers bins 255-8*lane-q (descending)
+      const int lane = threadIdx.x;
+      unsigned c8[8];
+      unsigned long long lsum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        c8[q] = s_h[255 - 8 * lane - q];
+        lsum += c8[q];
+      }
+      unsigned long long incl = lsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const unsigned long long excl = incl - lsum;
+      if (excl < rem && incl >= rem) {
+        unsigned long long cum = excl;
+        int b = -1;
+        unsigned cb = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (b < 0 && cum + c8[q] >= rem) {
+            b = 255 - 8 * lane - q;
+            cb = c8[q];
+          } else if (b < 0) {
+            cum += c8[q];
+          }
+        }
+        const unsigned long long nrem = rem - cum;
+        uint64_t ph = pre_hi;
+        uint32_t pl = pre_lo;
+        if (bits < 64) ph |= (uint64_t)b << (56 - bits);
+        else pl |= (uint32_t)b << (24 - (bits - 64));
+        sh_hi = ph;
+        sh_lo = pl;
+        sh_bits = bits + 8;
+        sh_rem = nrem;
+        sh_done = (nrem == cb) || (bits + 8 >= 96);
+      }
+    }
+    __syncthreads();
+    pre_hi = sh_hi;
+    pre_lo = sh_lo;
+    bits = sh_bits;
+    rem = sh_rem;
+    const int done = sh_done;
+    __syncthreads();
+    if (done) break;
+  }
+  *out_hi = pre_hi;
+  *out_lo = pre_lo;
+}
+
 __device__ __forceinline__ void rank_items(const uint64_t* s_hi, const uint32_t* s_lo, uint32_t m, uint64_t need,
                                            int mode, SelectCtl* ctl, uint32_t* out_rows, uint64_t* out_hi) {
   const unsigned lane = lane_id();
@@ -723,12 +810,8 @@ __global__ void __launch_bounds__(kSelThreads) topk_fused_kernel(FusedTopkArgs f
   static_assert(kSortTile >= kRankMax, "rank lists are staged in the select tile");
   cg::grid_group grid = cg::this_grid();
   const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
-  {  // zero the candidate and fallback controls (histograms, counters, status)
-    unsigned* z = reinterpret_cast<unsigned*>(f.ctl + 1);
-    const uint64_t words = 2 * sizeof(SelectCtl) / sizeof(unsigned);
-    for (uint64_t i = gtid; i < words; i += gstride) z[i] = 0u;
-  }
+  // (the candidate and fallback controls, ctl[1..2], are zeroed by the launch code:
+  // with no grid barrier before the filter, blocks may append candidates at once)
   const SrcSample smp{f.keys, f.rows, f.n, f.w};
   constexpr int kGather = kRankMax / kSelThreads;  // all loads of a thread in flight together
   {
@@ -752,10 +835,16 @@ __global__ void __launch_bounds__(kSelThreads) topk_fused_kernel(FusedTopkArgs f
     }
   }
   __syncthreads();
-  rank_items(s_hi, s_lo, f.s, f.need_s, kModeThreshold, f.ctl, nullptr, nullptr);
-  grid.sync();
-  const double tk = __ldcg(&f.ctl->thr_key);
-  const uint32_t tr = __ldcg(&f.ctl->thr_row);
+  // every block selects the same threshold from the same samples: no grid barrier
+  uint64_t t_hi;
+  uint32_t t_lo;
+  block_radix_threshold(s_hi, s_lo, f.s, f.need_s, &t_hi, &t_lo);
+  const double tk = key_from_ord(t_hi);
+  const uint32_t tr = ~t_lo;
+  if (gtid == 0) {
+    f.ctl->thr_key = tk;
+    f.ctl->thr_row = tr;
+  }
   filter_body(f.keys, f.rows, f.n, tk, tr, &f.ctl[1].cand_count, f.cand_hi, f.cand_lo, f.cap);
   grid.sync();
   const unsigned long long c = __ldcg(&f.ctl[1].cand_count);
