@@ -523,8 +523,12 @@ constexpr size_t kRankSmem = (size_t)kRankMax * (sizeof(uint64_t) + sizeof(uint3
 // digits): the largest prefix P (low bits zero) such that exactly `need` items
 // are >= P. Every block computes the same P from the same items, so the fused
 // Top-K needs no grid barrier to publish its threshold. Called by all threads.
+// s_lo is filled by fill_lo() only once a pass needs row bits (a key tie at the
+// threshold), so the common case stages keys alone.
+template <class FillLo>
 __device__ __forceinline__ void block_radix_threshold(const uint64_t* s_hi, const uint32_t* s_lo, uint32_t m,
-                                                      uint64_t need, uint64_t* out_hi, uint32_t* out_lo) {
+                                                      uint64_t need, uint64_t* out_hi, uint32_t* out_lo,
+                                                      FillLo fill_lo) {
   __shared__ unsigned s_h[256];
   __shared__ uint64_t sh_hi;
   __shared__ uint32_t sh_lo;
@@ -534,7 +538,12 @@ __device__ __forceinline__ void block_radix_threshold(const uint64_t* s_hi, cons
   uint32_t pre_lo = 0;
   int bits = 0;
   unsigned long long rem = need;
+  bool lo_ready = false;
   for (int pass = 0; pass < 12; ++pass) {
+    if (bits >= 64 && !lo_ready) {  // block-uniform
+      fill_lo();
+      lo_ready = true;
+    }
     for (int t = threadIdx.x; t < 256; t += blockDim.x) s_h[t] = 0;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
@@ -814,31 +823,27 @@ __global__ void __launch_bounds__(kSelThreads) topk_fused_kernel(FusedTopkArgs f
   // with no grid barrier before the filter, blocks may append candidates at once)
   const SrcSample smp{f.keys, f.rows, f.n, f.w};
   constexpr int kGather = kRankMax / kSelThreads;  // all loads of a thread in flight together
-  {
+  {  // sample keys (rows only if the threshold lands in a key tie, below)
     uint64_t h[kGather];
-    uint32_t l[kGather];
 #pragma unroll
     for (int u = 0; u < kGather; ++u) {
       const uint32_t i = threadIdx.x + u * kSelThreads;
-      if (i < f.s) {
-        h[u] = smp.hi(i);
-        l[u] = smp.lo(i);
-      }
+      if (i < f.s) h[u] = smp.hi(i);
     }
 #pragma unroll
     for (int u = 0; u < kGather; ++u) {
       const uint32_t i = threadIdx.x + u * kSelThreads;
-      if (i < f.s) {
-        s_hi[i] = h[u];
-        s_lo[i] = l[u];
-      }
+      if (i < f.s) s_hi[i] = h[u];
     }
   }
   __syncthreads();
   // every block selects the same threshold from the same samples: no grid barrier
   uint64_t t_hi;
   uint32_t t_lo;
-  block_radix_threshold(s_hi, s_lo, f.s, f.need_s, &t_hi, &t_lo);
+  block_radix_threshold(s_hi, s_lo, f.s, f.need_s, &t_hi, &t_lo, [&]() {
+    for (uint32_t i = threadIdx.x; i < f.s; i += blockDim.x) s_lo[i] = smp.lo(i);
+    __syncthreads();
+  });
   const double tk = key_from_ord(t_hi);
   const uint32_t tr = ~t_lo;
   if (gtid == 0) {
