@@ -552,8 +552,8 @@ int launch_rank(const SelectArgs<Src>& a, unsigned long long* clear_count, cudaS
 }
 
 int ensure_topk_ws(uint64_t kk, uint64_t cap) {
-  CK(g.w_hi.ensure(std::max<uint64_t>(kk, 1) * 8));
-  CK(g.w_lo.ensure(std::max<uint64_t>(kk, 1) * 4));
+  CK(g.w_hi.ensure(std::max<uint64_t>(kk, 1) * 16));  // winners + merge buffer
+  CK(g.w_lo.ensure(std::max<uint64_t>(kk, 1) * 8));
   if (cap) {
     CK(g.cand_hi.ensure(cap * 8));
     CK(g.cand_lo.ensure(cap * 4));

@@ -27,6 +27,14 @@ namespace cg = cooperative_groups;
 
 constexpr int kSelThreads = 1024;
 constexpr uint32_t kSortTile = 8192;  // items per shared-memory sort tile (96 KB)
+#ifndef GOLP_MERGE_TILE
+#define GOLP_MERGE_TILE 1024
+#endif
+#ifndef GOLP_MERGE_PER
+#define GOLP_MERGE_PER 1
+#endif
+constexpr uint32_t kMergeTile = GOLP_MERGE_TILE;  // winner sort: runs sorted per block before the merges
+constexpr uint32_t kMergePer = GOLP_MERGE_PER;    // winner sort: outputs per thread per merge round
 constexpr int kModeFull = 0;          // radix select + collect + sort + emit
 constexpr int kModeThreshold = 1;     // radix select only -> ctl->thr_*
 
@@ -91,7 +99,7 @@ struct SelectArgs {
   int use_cand_count;  // n := ctl->cand_count, validated against need/cap
   int mode;
   SelectCtl* ctl;
-  uint64_t* w_hi;      // winners scratch, >= need entries
+  uint64_t* w_hi;      // winners scratch, >= 2 * need entries (the second half: merge buffer)
   uint32_t* w_lo;
   uint32_t* out_rows;  // need entries, best first
   uint64_t* out_hi;    // optional: encoded keys of the winners (for merges)
@@ -426,12 +434,15 @@ __device__ void select_body(const SelectArgs<Src>& a) {
   uint64_t* gh = a.w_hi;
   uint32_t* gl = a.w_lo;
   const uint64_t m = need;
-  const uint64_t ntiles = (m + kSortTile - 1) / kSortTile;
-  const int logTile = ilog2_u64(kSortTile);
-  // (a) every tile sorted locally = all merge sizes up to kSortTile
+  // (a) runs of kMergeTile sorted in shared memory, one block per run (small
+  // runs keep every SM busy; a whole-block bitonic sort of 8192 was 120 µs)
+  const uint64_t ntiles = (m + kMergeTile - 1) / kMergeTile;
+#if GOLP_SEL_TIMING
+  const long long ttile = clock64();
+#endif
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t base = tile * kSortTile;
-    const uint32_t cnt = (uint32_t)((m - base) < kSortTile ? (m - base) : kSortTile);
+    const uint64_t base = tile * kMergeTile;
+    const uint32_t cnt = (uint32_t)((m - base) < kMergeTile ? (m - base) : kMergeTile);
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
       s_hi[i] = __ldcg(gh + base + i);
       s_lo[i] = __ldcg(gl + base + i);
@@ -444,55 +455,68 @@ __device__ void select_body(const SelectArgs<Src>& a) {
     }
     __syncthreads();
   }
+#if GOLP_SEL_TIMING
+  if (blockIdx.x == 0 && threadIdx.x == 0) printf("tile sort %lld cycles\n", clock64() - ttile);
+#endif
   grid.sync();
-  const int logP = ilog2_u64(next_pow2_u64(m));
-  const uint64_t pairs = (1ull << logP) >> 1;
-  for (int logk = logTile + 1; logk <= logP; ++logk) {
-    for (uint64_t t = gtid; t < pairs; t += gstride) {
-      uint64_t i, j;
-      flip_pair(t, logk, i, j);
-      if (j < m) {
-        const uint64_t hi_ = __ldcg(gh + i), hj = __ldcg(gh + j);
-        const uint32_t li = __ldcg(gl + i), lj = __ldcg(gl + j);
-        if (item_gt(hj, lj, hi_, li)) {
-          __stcg(gh + i, hj); __stcg(gh + j, hi_);
-          __stcg(gl + i, lj); __stcg(gl + j, li);
-        }
+#if GOLP_SEL_TIMING
+  const long long tsorted = clock64();
+#endif
+  // (b) sorted runs of kSortTile merged pairwise (merge path: every thread finds
+  // where its kMergePer outputs start by a binary search on its diagonal, then
+  // merges them sequentially), ping-ponging with the second half of the winners
+  // scratch: ceil(log2(m / kSortTile)) rounds, one grid barrier each.
+  uint64_t* sh = gh;
+  uint32_t* sl = gl;
+  uint64_t* dh = gh + m;
+  uint32_t* dl = gl + m;
+  for (uint64_t L = kMergeTile; L < m; L <<= 1) {
+    const uint64_t nchunks = (m + kMergePer - 1) / kMergePer;
+    for (uint64_t c = gtid; c < nchunks; c += gstride) {
+      const uint64_t o0 = c * kMergePer;
+      const uint64_t base = (o0 / (2 * L)) * (2 * L);
+      const uint64_t la = base + L < m ? L : m - base;
+      const uint64_t b0 = base + la;
+      const uint64_t lb = b0 < m ? (b0 + L < m ? L : m - b0) : 0;
+      const uint64_t k = o0 - base;
+      // smallest i (items taken from run A among the first k) such that A[i]
+      // does not go before B[k - i - 1]; A wins ties (item_gt is strict)
+      uint64_t lo = k > lb ? k - lb : 0, hi = k < la ? k : la;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        const uint64_t bj = b0 + (k - mid - 1);
+        if (!item_gt(__ldcg(sh + bj), __ldcg(sl + bj), __ldcg(sh + base + mid), __ldcg(sl + base + mid))) lo = mid + 1;
+        else hi = mid;
+      }
+      uint64_t i = lo, j = k - lo;
+      const uint64_t end = (o0 + kMergePer < base + la + lb) ? o0 + kMergePer : base + la + lb;
+      for (uint64_t o = o0; o < end; ++o) {
+        bool take_a;
+        if (i >= la) take_a = false;
+        else if (j >= lb) take_a = true;
+        else take_a = !item_gt(__ldcg(sh + b0 + j), __ldcg(sl + b0 + j), __ldcg(sh + base + i), __ldcg(sl + base + i));
+        const uint64_t src = take_a ? base + i : b0 + j;
+        __stcg(dh + o, __ldcg(sh + src));
+        __stcg(dl + o, __ldcg(sl + src));
+        if (take_a) ++i;
+        else ++j;
       }
     }
     grid.sync();
-    for (int logs = logk - 2; logs >= logTile; --logs) {
-      for (uint64_t t = gtid; t < pairs; t += gstride) {
-        uint64_t i, j;
-        half_pair(t, logs, i, j);
-        if (j < m) {
-          const uint64_t hi_ = __ldcg(gh + i), hj = __ldcg(gh + j);
-          const uint32_t li = __ldcg(gl + i), lj = __ldcg(gl + j);
-          if (item_gt(hj, lj, hi_, li)) {
-            __stcg(gh + i, hj); __stcg(gh + j, hi_);
-            __stcg(gl + i, lj); __stcg(gl + j, li);
-          }
-        }
-      }
-      grid.sync();
-    }
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const uint64_t base = tile * kSortTile;
-      const uint32_t cnt = (uint32_t)((m - base) < kSortTile ? (m - base) : kSortTile);
-      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-        s_hi[i] = __ldcg(gh + base + i);
-        s_lo[i] = __ldcg(gl + base + i);
-      }
-      __syncthreads();
-      block_half_steps_desc(s_hi, s_lo, cnt, logTile - 1, kSortTile / 2);
-      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-        __stcg(gh + base + i, s_hi[i]);
-        __stcg(gl + base + i, s_lo[i]);
-      }
-      __syncthreads();
-    }
-    grid.sync();
+    uint64_t* th = sh;
+    uint32_t* tl = sl;
+    sh = dh;
+    sl = dl;
+    dh = th;
+    dl = tl;
   }
+  gh = sh;
+  gl = sl;
+#if GOLP_SEL_TIMING
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("winner sort: m %llu tiles %llu cycles, merges %lld cycles\n", (unsigned long long)m,
+           (unsigned long long)ntiles, clock64() - tsorted);
+#endif
   for (uint64_t i = gtid; i < m; i += gstride) {
     a.out_rows[i] = ~__ldcg(gl + i);
     if (a.out_hi) a.out_hi[i] = __ldcg(gh + i);
