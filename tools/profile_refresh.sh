@@ -12,3 +12,6 @@ echo c4 rc=$?
 ncu --set full --clock-control none --import-source on -k regex:"join_probe_part_kernel" -c 1 \
   -o gpurun_out/full_c4span_probe_part python tools/join_breakdown.py 1e8 268435456 2e8 1 > gpurun_out/full_c4span.log 2>&1
 echo full rc=$?
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"select|filter|topk|rank" --csv \
+  python bench.py --workload topk_c1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/launches_topk_c1_fused.csv 2>&1
+echo c1 rc=$?
