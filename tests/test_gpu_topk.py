@@ -186,3 +186,26 @@ def test_topk_large_uniform_known_properties(cuda):
         out, _ = resident.topk(tk, tr, k)
         got = out.cpu().numpy().view(np.uint32)
         assert np.array_equal(got, oracle.topk(keys, rows, k)), k
+
+
+@pytest.mark.parametrize("k,parts,domain", [(20_000, 4, 1 << 40), (50_000, 3, 5000), (8193, 2, 1 << 20)])
+def test_topk_large_k_local_and_merge(cuda, k, parts, domain):
+    """K above one shared-memory sort tile: the winners are sorted as 1024-item runs
+    plus merge-path rounds, both in the local Top-K and in the cross-shard merge."""
+    import torch
+
+    from paper_2601_19911_b200 import resident
+
+    rng = np.random.default_rng(k + parts)
+    n = 3_000_000
+    keys = rng.integers(0, domain, size=n).astype(np.float64)
+    rows = rng.permutation(n).astype(np.uint32)
+    tk = torch.from_numpy(keys).to(cuda)
+    tr = torch.from_numpy(rows.view(np.int32)).to(cuda)
+    expect = oracle.topk(keys, rows, k)
+    out, _ = resident.topk(tk, tr, k, want_codes=True)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), expect)
+    bounds = np.linspace(0, n, parts + 1).astype(int)
+    res = [resident.topk(tk[a:b], tr[a:b], k, want_codes=True) for a, b in zip(bounds[:-1], bounds[1:])]
+    merged, _ = resident.merge(torch.cat([r[1] for r in res]), torch.cat([r[0] for r in res]), k)
+    assert np.array_equal(merged.cpu().numpy().view(np.uint32), expect)
