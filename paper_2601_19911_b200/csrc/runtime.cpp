@@ -1,5 +1,7 @@
 #include "runtime.h"
 
+#include <cstdlib>
+
 namespace golp {
 
 static std::mutex g_err_mu;
@@ -23,6 +25,7 @@ double wall_seconds() {
 void WorkerPool::start(int workers) {
   stop();
   stop_ = false;
+  if (const char* v = std::getenv("GOLP_POOL_SPIN_US")) spin_s_ = std::atof(v) * 1e-6;
   for (int i = 0; i < workers; ++i) threads_.emplace_back([this] { loop(); });
 }
 
@@ -36,20 +39,41 @@ void WorkerPool::stop() {
   threads_.clear();
 }
 
+// Idle workers spin on the job generation for spin_s_ before blocking, so the
+// back-to-back jobs of one offload call (a row check or staging copy per chunk)
+// do not each pay a futex wake-up; a worker that blocks counts itself in
+// sleepers_ and run() only notifies when somebody sleeps.
 void WorkerPool::loop() {
   uint64_t seen = 0;
   while (true) {
-    const std::function<void(size_t)>* job;
-    {
-      std::unique_lock<std::mutex> lk(mu_);
-      cv_work_.wait(lk, [&] { return stop_ || gen_ != seen; });
-      if (stop_) return;
-      seen = gen_;
-      job = job_;
+    const double t0 = wall_seconds();
+    unsigned spins = 0;
+    while (gen_.load() == seen && !stop_.load()) {
+      if ((++spins & 63u) == 0 && wall_seconds() - t0 > spin_s_) {
+        std::unique_lock<std::mutex> lk(mu_);
+        sleepers_.fetch_add(1);
+        cv_work_.wait(lk, [&] { return stop_.load() || gen_.load() != seen; });
+        sleepers_.fetch_sub(1);
+        break;
+      }
+#if defined(__x86_64__)
+      __builtin_ia32_pause();
+#endif
     }
-    for (size_t i = next_.fetch_add(1); i < total_; i = next_.fetch_add(1)) (*job)(i);
-    std::lock_guard<std::mutex> lk(mu_);
-    if (--pending_ == 0) cv_done_.notify_all();
+    if (stop_.load()) return;
+    const std::function<void(size_t)>* job;
+    size_t total;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      seen = gen_.load();
+      job = job_;
+      total = total_;
+    }
+    for (size_t i = next_.fetch_add(1); i < total; i = next_.fetch_add(1)) (*job)(i);
+    if (pending_.fetch_sub(1) == 1) {
+      std::lock_guard<std::mutex> lk(mu_);
+      cv_done_.notify_all();
+    }
   }
 }
 
@@ -63,13 +87,24 @@ void WorkerPool::run(size_t ntasks, const std::function<void(size_t)>& fn) {
     job_ = &fn;
     total_ = ntasks;
     next_.store(0);
-    pending_ = (int)threads_.size();
-    ++gen_;
+    pending_.store((int)threads_.size());
+    gen_.fetch_add(1);
   }
-  cv_work_.notify_all();
+  if (sleepers_.load() > 0) cv_work_.notify_all();
   for (size_t i = next_.fetch_add(1); i < ntasks; i = next_.fetch_add(1)) fn(i);
-  std::unique_lock<std::mutex> lk(mu_);
-  cv_done_.wait(lk, [&] { return pending_ == 0; });
+  // every worker checks in (a late one must not read the next job's state)
+  const double t0 = wall_seconds();
+  unsigned spins = 0;
+  while (pending_.load() != 0) {
+    if ((++spins & 63u) == 0 && wall_seconds() - t0 > spin_s_) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_done_.wait(lk, [&] { return pending_.load() == 0; });
+      break;
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
 }
 
 void parallel_copy(WorkerPool& pool, void* dst, const void* src, size_t bytes) {

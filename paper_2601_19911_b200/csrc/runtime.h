@@ -35,9 +35,11 @@ class WorkerPool {
   const std::function<void(size_t)>* job_ = nullptr;
   size_t total_ = 0;
   std::atomic<size_t> next_{0};
-  int pending_ = 0;
-  uint64_t gen_ = 0;
-  bool stop_ = false;
+  std::atomic<int> pending_{0};
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> sleepers_{0};
+  std::atomic<bool> stop_{false};
+  double spin_s_ = 200e-6;  // idle workers spin this long before sleeping (GOLP_POOL_SPIN_US)
 };
 
 // memcpy split across the pool (the packer's inner loop).
