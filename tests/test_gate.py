@@ -193,3 +193,70 @@ def test_scaling_baseline_host_wall_clock_rows():
     rows = run_scaling_baseline(WorkloadSpec(n_grid=(100, 2_000), k=10, repeats=2), backend="host")
     assert [(r.n, r.op) for r in rows] == [(100, "full_sort"), (100, "topk"), (2_000, "full_sort"), (2_000, "topk")]
     assert all(0 < r.median_s <= r.p95_s for r in rows)
+
+
+# ---- opt-in K-aware host cost terms (not in the reference; defaults keep its model) ----
+
+
+def test_k_aware_fields_default_to_the_reference_model():
+    m = CpuCostModel(1e-10, 5e-6, 5e-10, 5e-6)
+    assert not m.k_aware
+    assert set(m.to_json_dict()) == {"alpha_sort", "beta_sort", "alpha_match", "beta_match"}
+    for op, n, k in ((OP_TOPK, 10**6, 10**5), (OP_PROBE, 10**4, 500)):
+        ref = (1e-10 * n * math.log2(n) + 5e-6) if op == OP_TOPK else (5e-10 * n * k + 5e-6)
+        assert estimate_cpu_cost(m, op, n, k) == ref
+    ext = CpuCostModel(1e-10, 5e-6, 5e-10, 5e-6, alpha_topk_k=3e-9, alpha_pair=2e-9)
+    assert ext.k_aware and CpuCostModel.from_json_dict(ext.to_json_dict()) == ext
+    assert CpuCostModel.from_json_dict(m.to_json_dict()) == m
+    with pytest.raises(ValueError):
+        CpuCostModel(1e-10, 5e-6, 5e-10, 5e-6, alpha_pair=-1.0)
+
+
+def test_k_aware_estimates():
+    ext = CpuCostModel(1e-10, 5e-6, 5e-10, 5e-6, alpha_topk_k=3e-9, alpha_pair=2e-9)
+    n, k = 10**6, 10**5
+    assert estimate_cpu_cost(ext, OP_TOPK, n, k) == pytest.approx(
+        1e-10 * n * math.log2(n) + 3e-9 * k * math.log2(k) + 5e-6, rel=1e-15)
+    # K is clamped to n: K >= n costs what K = n costs
+    assert estimate_cpu_cost(ext, OP_TOPK, 1000, 10**6) == estimate_cpu_cost(ext, OP_TOPK, 1000, 1000)
+    # probes are linear in n and M instead of n * M
+    assert estimate_cpu_cost(ext, OP_PROBE, 1000, 500) == pytest.approx(5e-10 * 1000 + 2e-9 * 500 + 5e-6)
+
+
+def test_k_aware_calibration_recovers_the_generating_constants():
+    a_s, a_k, b_s, a_m, a_p, b_m = 4e-11, 2e-9, 3e-6, 7e-9, 1.5e-8, 4e-6
+    samples = []
+    for n in (10**4, 10**5, 10**6, 4 * 10**6):
+        for k in (10, 1000, 10**5):
+            kk = min(k, n)
+            samples.append((OP_TOPK, n, k, a_s * n * math.log2(n) + a_k * kk * math.log2(max(kk, 2)) + b_s))
+    for n in (10**4, 10**5, 10**6):
+        for m in (1, n // 2):
+            samples.append((OP_PROBE, n, m, a_m * n + a_p * m + b_m))
+    got = calibrate_cpu_model(samples, k_aware=True)
+    for name, want in (("alpha_sort", a_s), ("alpha_topk_k", a_k), ("beta_sort", b_s), ("alpha_match", a_m),
+                       ("alpha_pair", a_p), ("beta_match", b_m)):
+        assert getattr(got, name) == pytest.approx(want, rel=1e-6), name
+    # the reference fit of the same samples is unchanged by the option
+    assert not calibrate_cpu_model(samples).k_aware
+
+
+def test_k_aware_calibration_needs_two_k_values():
+    samples = [(OP_TOPK, n, 100, 1e-9 * n) for n in (10**4, 10**5, 10**6)]
+    with pytest.raises(CalibrationError):
+        calibrate_cpu_model(samples, k_aware=True)
+    assert calibrate_cpu_model(samples).alpha_sort > 0.0
+
+
+def test_k_aware_gate_fixes_the_reference_forms_misses():
+    """The two miss patterns of profiles/r1_gate_cells.json: Top-K with a large K
+    stays on the host under n*log(n), and a tiny probe with a large M goes to the
+    device under n*M. The K-aware terms move both the other way."""
+    prof = DeviceProfile(5e10, 5e10, 5e-5, 1e-12, 1e-12, 1e-9)
+    ref = CpuCostModel(4.3e-11, 0.0, 7.8e-9, 0.0)
+    ext = CpuCostModel(4.3e-11, 0.0, 7.8e-9, 0.0, alpha_topk_k=6e-9, alpha_pair=1e-9)
+    n, k = 10**5, 10**5
+    assert decide(GateConfig(cpu_model=ref, profile=prof), OP_TOPK, n, k).path == HOST
+    assert decide(GateConfig(cpu_model=ext, profile=prof), OP_TOPK, n, k).path == DEVICE
+    assert decide(GateConfig(cpu_model=ref, profile=prof), OP_PROBE, 1000, 500, None, 100).path == DEVICE
+    assert decide(GateConfig(cpu_model=ext, profile=prof), OP_PROBE, 1000, 500, None, 100).path == HOST

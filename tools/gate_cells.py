@@ -23,6 +23,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2601_19911_b200 import (  # noqa: E402
     B200Device, FULL_ROW, KEY_ONLY, OP_PROBE, OP_TOPK, GateConfig, calibrate_cpu_model, host_topk,
     random_key_vector)
+from paper_2601_19911_b200.store import KeyVector  # noqa: E402
 from paper_2601_19911_b200.gate import DEVICE, HOST, execute_gated, execute_path  # noqa: E402
 from paper_2601_19911_b200.harness import calibrate_device_profile, compute_stats, table_seed  # noqa: E402
 from paper_2601_19911_b200.host import host_hash_build, host_hash_probe  # noqa: E402
@@ -49,23 +50,30 @@ def probe_tables(n, payload, seed):
     return ColumnTable(bk, pay(nb), seed), ColumnTable(pk, pay(n), seed + 1)
 
 
-def run_cell(tables, op, k, cfg, dev, reps):
+def run_cell(tables, op, k, cfg, dev, reps, cfg_k=None):
     """Warm each path twice (B200Device page-locks a reused input column on its
     second call, a one-off ~0.1-0.4 s at 1e8 rows that a query stream amortizes),
     then interleave host / device / gated per repeat."""
     for _ in range(2):
         for path in (HOST, DEVICE):
             execute_path(tables, op, k, cfg, dev, path)
-    host, devt, gated = [], [], []
-    choice = None
+    host, devt, gated, gated_k = [], [], [], []
+    choice = choice_k = None
     for _ in range(reps):
         host.append(execute_path(tables, op, k, cfg, dev, HOST)[1])
         devt.append(execute_path(tables, op, k, cfg, dev, DEVICE)[1])
         _, decision, t = execute_gated(tables, op, k, cfg, dev)
         gated.append(t)
         choice = decision.path
-    return {"cpu_only": stats(host), "always_on": stats(devt), "gated": stats(gated), "gate_choice": choice,
-            "repeats": reps}
+        if cfg_k is not None:
+            _, decision, t = execute_gated(tables, op, k, cfg_k, dev)
+            gated_k.append(t)
+            choice_k = decision.path
+    out = {"cpu_only": stats(host), "always_on": stats(devt), "gated": stats(gated), "gate_choice": choice,
+           "repeats": reps}
+    if cfg_k is not None:
+        out.update({"gated_k_aware": stats(gated_k), "gate_choice_k_aware": choice_k})
+    return out
 
 
 def main(out_path, max_n):
@@ -88,6 +96,23 @@ def main(out_path, max_n):
         bkv, pkv = extract_keys(b), extract_keys(p)
         samples.append((OP_PROBE, n, 1, _time(lambda: host_hash_probe(host_hash_build(bkv), pkv))))
     cpu = calibrate_cpu_model(samples)
+    # K-aware extension (CpuCostModel.alpha_topk_k / alpha_pair; not the reference's
+    # form): Top-K samples at several K, probe samples at two match rates so that n and
+    # M separate (the second probe side draws its keys outside the build domain, M = 0).
+    k_samples = []
+    for n in (100_000, 1_000_000, 4_000_000, 16_000_000):
+        kv = random_key_vector(n, n)
+        for k in (10, 1000, 100_000):
+            k_samples.append((OP_TOPK, n, k, _time(lambda: host_topk(kv, k))))
+    for n in (100_000, 1_000_000, 4_000_000):
+        b, p = probe_tables(n, 1, n)
+        bkv, pkv = extract_keys(b), extract_keys(p)
+        ht = host_hash_build(bkv)
+        m = len(host_hash_probe(ht, pkv).probe_rows)
+        k_samples.append((OP_PROBE, n, m, _time(lambda: host_hash_probe(host_hash_build(bkv), pkv))))
+        miss = KeyVector(pkv.keys + 4.0 * len(bkv), pkv.rows)
+        k_samples.append((OP_PROBE, n, 0, _time(lambda: host_hash_probe(host_hash_build(bkv), miss))))
+    cpu_k = calibrate_cpu_model(k_samples, k_aware=True)
     cells = []
     ns = [n for n in (1_000, 10_000, 100_000, 1_000_000, 10_000_000, 100_000_000) if n <= max_n]
     for n in ns:
@@ -96,20 +121,21 @@ def main(out_path, max_n):
                 continue  # 196 B/row: 19.6 GB per call at 1e8 -- host RAM, not the device, is the limit
             payload = 188 if mode == FULL_ROW else 1  # key-only never ships the payload
             cfg = GateConfig(mode=mode, profile=prof, cpu_model=cpu)
+            cfg_k = GateConfig(mode=mode, profile=prof, cpu_model=cpu_k)
             table = generate_table(n, payload_bytes=payload, seed=table_seed(7, n),
                                    memory_budget=1 << 40)
             for k in (10, 1000, 100_000):
                 if k > n:
                     continue
                 cell = {"op": OP_TOPK, "n": n, "k": k, "mode": mode}
-                cell.update(run_cell(table, OP_TOPK, k, cfg, dev, repeats_for(n)))
+                cell.update(run_cell(table, OP_TOPK, k, cfg, dev, repeats_for(n), cfg_k))
                 cells.append(cell)
                 print(json.dumps(cell), flush=True)
             del table
             tables = probe_tables(n, payload, table_seed(9, n))
             for m in (1, n // 2):  # the gate's M: a point estimate and the expected match count
                 cell = {"op": OP_PROBE, "n": n, "build_n": tables[0].row_count, "m": m, "mode": mode}
-                cell.update(run_cell(tables, OP_PROBE, max(m, 1), cfg, dev, repeats_for(n)))
+                cell.update(run_cell(tables, OP_PROBE, max(m, 1), cfg, dev, repeats_for(n), cfg_k))
                 cells.append(cell)
                 print(json.dumps(cell), flush=True)
     # per cell, how the gate's percentiles compare with the better fixed strategy
@@ -117,8 +143,9 @@ def main(out_path, max_n):
         for q in ("p95", "p99"):
             best = min(c["cpu_only"][q], c["always_on"][q])
             c[f"gated_{q}_over_best_fixed"] = c["gated"][q] / best if best > 0 else None
-    out = {"profile_b200": prof.to_json_dict(), "cpu_model_host_engine": cpu.to_json_dict(), "cells": cells,
-           "wall_s": time.time() - t0}
+            c[f"gated_k_aware_{q}_over_best_fixed"] = c["gated_k_aware"][q] / best if best > 0 else None
+    out = {"profile_b200": prof.to_json_dict(), "cpu_model_host_engine": cpu.to_json_dict(),
+           "cpu_model_host_engine_k_aware": cpu_k.to_json_dict(), "cells": cells, "wall_s": time.time() - t0}
     Path(out_path).write_text(json.dumps(out, indent=1))
     dev.close()
 

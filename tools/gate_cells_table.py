@@ -16,3 +16,25 @@ for c in d["cells"]:
     print(f"{c['op']:5s} n={c['n']:>11,} {'k' if 'k' in c else 'm'}={kk:>10,} {c['mode']:8s} cpu {f(c['cpu_only'])} "
           f"dev {f(c['always_on'])} gated {f(c['gated'])} -> {c['gate_choice']:6s} "
           f"p95x {c['gated_p95_over_best_fixed']:.2f} p99x {c['gated_p99_over_best_fixed']:.2f}")
+
+if "cpu_model_host_engine_k_aware" in d:
+    print("cpu k-aware", d["cpu_model_host_engine_k_aware"])
+    for c in d["cells"]:
+        kk = c.get("k", c.get("m"))
+        print(f"{c['op']:5s} n={c['n']:>11,} {kk:>10,} {c['mode']:8s} k-aware gated {f(c['gated_k_aware'])} -> "
+              f"{c['gate_choice_k_aware']:6s} p95x {c['gated_k_aware_p95_over_best_fixed']:.2f} "
+              f"p99x {c['gated_k_aware_p99_over_best_fixed']:.2f}")
+
+
+def summary(tag, choice_key, prefix):
+    cells = d["cells"]
+    if choice_key not in cells[0]:
+        return
+    right = sum((c[choice_key] == "device") == (c["always_on"]["p50"] < c["cpu_only"]["p50"]) for c in cells)
+    le95 = sum(c[f"{prefix}p95_over_best_fixed"] <= 1.0 for c in cells)
+    w5 = sum(c[f"{prefix}p95_over_best_fixed"] <= 1.05 for c in cells)
+    print(f"{tag}: faster path chosen in {right}/{len(cells)} cells; P95 <= best fixed in {le95}, within 5% in {w5}")
+
+
+summary("reference form", "gate_choice", "gated_")
+summary("K-aware", "gate_choice_k_aware", "gated_k_aware_")
