@@ -18,7 +18,7 @@ for c in d["cells"]:
           f"p95x {c['gated_p95_over_best_fixed']:.2f} p99x {c['gated_p99_over_best_fixed']:.2f}")
 
 if "cpu_model_host_engine_k_aware" in d:
-    print("cpu k-aware", d["cpu_model_host_engine_k_aware"])
+    print("cpu k-aware", d["cpu_model_host_engine_k_aware"], "margin_s", d.get("margin_s_k_aware"))
     for c in d["cells"]:
         kk = c.get("k", c.get("m"))
         print(f"{c['op']:5s} n={c['n']:>11,} {kk:>10,} {c['mode']:8s} k-aware gated {f(c['gated_k_aware'])} -> "
