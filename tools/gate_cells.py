@@ -23,11 +23,16 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2601_19911_b200 import (  # noqa: E402
     B200Device, FULL_ROW, KEY_ONLY, OP_PROBE, OP_TOPK, GateConfig, calibrate_cpu_model, host_topk,
     random_key_vector)
-from paper_2601_19911_b200.store import KeyVector  # noqa: E402
 from paper_2601_19911_b200.gate import DEVICE, HOST, execute_gated, execute_path  # noqa: E402
 from paper_2601_19911_b200.harness import calibrate_device_profile, compute_stats, table_seed  # noqa: E402
 from paper_2601_19911_b200.host import host_hash_build, host_hash_probe  # noqa: E402
 from paper_2601_19911_b200.store import ColumnTable, extract_keys, generate_table  # noqa: E402
+
+
+# A query stream does not call the host engine back to back: its worker pool has gone
+# idle (spin, then futex sleep) by the next query. The K-aware calibration idles this
+# long before each timed host query so it pays the same wake-up as the cells do.
+IDLE_S = 0.002
 
 
 def repeats_for(n):
@@ -97,21 +102,25 @@ def main(out_path, max_n):
         samples.append((OP_PROBE, n, 1, _time(lambda: host_hash_probe(host_hash_build(bkv), pkv))))
     cpu = calibrate_cpu_model(samples)
     # K-aware extension (CpuCostModel.alpha_topk_k / alpha_pair; not the reference's
-    # form): Top-K samples at several K, probe samples at two match rates so that n and
-    # M separate (the second probe side draws its keys outside the build domain, M = 0).
+    # form), calibrated on the query the gate decides: execute_path's host wall time
+    # (extract_keys + engine + materialize), not the bare engine call. Top-K samples at
+    # several K; probe samples at two match rates so that n and M separate (the second
+    # probe side draws its keys outside the build domain, M = 0).
     k_samples = []
+    cfg_h = GateConfig(profile=prof, cpu_model=cpu)
     for n in (1_000, 10_000, 100_000, 1_000_000, 4_000_000, 16_000_000):
-        kv = random_key_vector(n, n)
+        t = generate_table(n, payload_bytes=1, seed=table_seed(5, n), memory_budget=1 << 40)
         for k in (10, 1000, 100_000):
-            k_samples.append((OP_TOPK, n, k, _time(lambda: host_topk(kv, k), 9 if n <= 10_000 else 3)))
+            k_samples.append((OP_TOPK, n, k, _time(lambda: execute_path(t, OP_TOPK, k, cfg_h, dev, HOST),
+                                                   9 if n <= 10_000 else 3, IDLE_S)))
     for n in (1_000, 10_000, 100_000, 1_000_000, 4_000_000):
         b, p = probe_tables(n, 1, n)
-        bkv, pkv = extract_keys(b), extract_keys(p)
-        ht = host_hash_build(bkv)
-        m = len(host_hash_probe(ht, pkv).probe_rows)
-        k_samples.append((OP_PROBE, n, m, _time(lambda: host_hash_probe(host_hash_build(bkv), pkv), 9 if n <= 10_000 else 3)))
-        miss = KeyVector(pkv.keys + 4.0 * len(bkv), pkv.rows)
-        k_samples.append((OP_PROBE, n, 0, _time(lambda: host_hash_probe(host_hash_build(bkv), miss), 9 if n <= 10_000 else 3)))
+        m = len(host_hash_probe(host_hash_build(extract_keys(b)), extract_keys(p)).probe_rows)
+        k_samples.append((OP_PROBE, n, m, _time(lambda: execute_path((b, p), OP_PROBE, 1, cfg_h, dev, HOST),
+                                                9 if n <= 10_000 else 3, IDLE_S)))
+        miss = ColumnTable(p.key_column + 4.0 * b.row_count, p.payload_column, n + 1)
+        k_samples.append((OP_PROBE, n, 0, _time(lambda: execute_path((b, miss), OP_PROBE, 1, cfg_h, dev, HOST),
+                                                9 if n <= 10_000 else 3, IDLE_S)))
     cpu_k = calibrate_cpu_model(k_samples, k_aware=True)
     # The profile is fitted on call ledgers, which leave out the per-query host work
     # around the call (extract_keys, materialize, Python). The K-aware gate charges it
@@ -159,9 +168,11 @@ def main(out_path, max_n):
     dev.close()
 
 
-def _time(fn, reps=3):
+def _time(fn, reps=3, idle_s=0.0):
     ts = []
     for _ in range(reps):
+        if idle_s:
+            time.sleep(idle_s)
         a = time.perf_counter()
         fn()
         ts.append(time.perf_counter() - a)
