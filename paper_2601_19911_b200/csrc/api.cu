@@ -803,7 +803,7 @@ int partition_entries(const double* keys, uint64_t n, bool probe_side, cudaStrea
   unsigned long long* cnt = g.part_cnt.as<unsigned long long>();
   unsigned long long* cur = g.part_cur.as<unsigned long long>();
   CK(cudaMemsetAsync(cnt, 0, P * 8, s));
-  part_count_kernel<<<g.sms * 2, kPartThreads, 0, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cnt);
+  part_count_kernel<<<g.sms * 4, kPartThreads, 0, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cnt);
   CKL();
   part_scan_kernel<<<1, 1024, 0, s>>>(cnt, cur, P);
   CKL();

@@ -548,12 +548,12 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(const double* 
   const uint64_t n2 = n / 2;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < n2; i += 4 * stride) {  // 4 independent 16-byte loads in flight
-    double2 v[4];
+  for (; i + 7 * stride < n2; i += 8 * stride) {  // 8 independent 16-byte loads in flight
+    double2 v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = ldg_stream_d2(keys + 2 * (i + u * stride), pol);
+    for (int u = 0; u < 8; ++u) v[u] = ldg_stream_d2(keys + 2 * (i + u * stride), pol);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       atomicAdd(&s_h[part_of(v[u].x, mask, slice_bits)], 1u);
       atomicAdd(&s_h[part_of(v[u].y, mask, slice_bits)], 1u);
     }
