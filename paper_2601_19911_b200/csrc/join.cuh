@@ -489,7 +489,10 @@ __global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(unsigned lo
 #ifndef GOLP_PART_MINB
 #define GOLP_PART_MINB 2
 #endif
-constexpr uint32_t kPartTile = 4096;  // entries per partition tile (run tables, match tiles)
+#ifndef GOLP_PART_TILE
+#define GOLP_PART_TILE 4096
+#endif
+constexpr uint32_t kPartTile = GOLP_PART_TILE;  // entries per partition tile (run tables, match tiles)
 constexpr int kPartThreads = GOLP_PART_THREADS;
 constexpr int kPartItems = (int)(kPartTile / kPartThreads);
 static_assert(kPartItems * kPartThreads == (int)kPartTile && kPartItems % 2 == 0, "tile split");
