@@ -13,10 +13,20 @@
  *     (streams are passed as an opaque `void*` = cudaStream_t, NULL = default);
  *   - every function returns a golp_status; golp_last_error() describes the
  *     last failure of the calling process;
- *   - calls are externally synchronous, one call at a time per process, exactly
- *     like the reference's ProxyDevice ("one call, one ledger");
+ *   - work runs on a CONTEXT bound to one CUDA device (streams, pinned staging,
+ *     HBM workspace). Each host thread has a current context: golp_init /
+ *     golp_use_device select a device's default context, golp_context_open
+ *     creates an independent one; a thread that selected none uses the default
+ *     context of its current CUDA device. Calls are externally synchronous per
+ *     context, exactly like the reference's ProxyDevice ("one call, one
+ *     ledger"); threads on different contexts run concurrently
+ *     (the G-GPU sharding of B200Device(gpus=G), ProxyDevice's chunk workers
+ *     at device.py:308-327 with GPUs as the workers);
  *   - the library never writes to input buffers and never retains input
- *     pointers after a call returns.
+ *     pointers after a call returns. (Page-locking a caller buffer for reuse
+ *     is an explicit request, golp_host_register; the Python B200Device's
+ *     PinCache makes it for columns it sees repeatedly -- pin_inputs=False
+ *     turns that off.)
  */
 #ifndef GOLP_B200_H
 #define GOLP_B200_H
@@ -72,11 +82,24 @@ typedef struct golp_kernel_times {
 /* ---- lifecycle ---------------------------------------------------------------- */
 const char* golp_last_error(void);
 int golp_version(void);
-/* Select the CUDA device and size the pinned staging ring (0 = defaults).
- * Replaces ProxyDevice.__init__ (device.py:308-310). Implicit on first use. */
+/* Make the default context of `device` (-1: the calling thread's current CUDA
+ * device) current on this thread, creating it with a pinned staging ring of
+ * pinned_chunk_bytes per slot and host_threads packer threads (0 = defaults)
+ * on first use. Replaces ProxyDevice.__init__ (device.py:308-310). Implicit on
+ * first use. */
 int golp_init(int device, uint64_t pinned_chunk_bytes, int host_threads);
-/* Frees device buffers, pinned staging and streams. Replaces
- * ProxyDevice.close (device.py:312-315). */
+/* golp_init(device, 0, 0): select device's default context on this thread. */
+int golp_use_device(int device);
+/* Device of the calling thread's current context (initializing it if needed). */
+int golp_current_device(int* device);
+/* An independent context on `device` (its own streams, staging and workspace),
+ * made current on this thread; *handle names it for golp_context_use/close. */
+int golp_context_open(int device, uint64_t pinned_chunk_bytes, int host_threads, int* handle);
+int golp_context_use(int handle);
+int golp_context_close(int handle);
+/* Frees every context's device buffers, pinned staging and streams. Replaces
+ * ProxyDevice.close (device.py:312-315). A context used again afterwards is
+ * re-initialized on its device. */
 int golp_shutdown(void);
 /* Number of CUDA kernels this library has launched (process lifetime). */
 uint64_t golp_launch_count(void);
@@ -128,11 +151,17 @@ int golp_host_free(void* ptr, uint64_t bytes);
 /* Page-lock a caller buffer in place (read-only) so that transfers of it skip
  * the staging copy; for columns reused across calls (registration is slow). */
 int golp_host_register(const void* ptr, uint64_t bytes);
-/* 1 when ptr is page-locked host memory the DMA engines can use directly. */
+/* 1 when ptr lies in page-locked host memory this library allocated
+ * (golp_host_alloc) or registered (golp_host_register). */
 int golp_host_is_pinned(const void* ptr);
+/* 1 when all of [ptr, ptr+bytes) lies in ONE such range: only then does a
+ * transfer of it skip the staging ring. */
+int golp_host_is_pinned_range(const void* ptr, uint64_t bytes);
 int golp_host_unregister(const void* ptr);
 
 /* ---- device-resident entry points (inputs already in HBM) ---------------------- */
+/* Device-resident entry points run on the calling thread's context and fail
+ * with GOLP_ERR_INVALID when the first input pointer lives on another device. */
 /* Top-K of n device-resident items. d_out_rows gets min(k, n) rows best first;
  * d_out_keys (optional, may be NULL) gets their order-preserving u64 key codes
  * (for cross-GPU merges via golp_topk_merge_device). */

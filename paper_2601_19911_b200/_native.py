@@ -65,6 +65,11 @@ SIGNATURES = {
     "golp_last_error": (C.c_char_p, []),
     "golp_version": (_int, []),
     "golp_init": (_int, [_int, _u64, _int]),
+    "golp_use_device": (_int, [_int]),
+    "golp_current_device": (_int, [C.POINTER(_int)]),
+    "golp_context_open": (_int, [_int, _u64, _int, C.POINTER(_int)]),
+    "golp_context_use": (_int, [_int]),
+    "golp_context_close": (_int, [_int]),
     "golp_shutdown": (_int, []),
     "golp_launch_count": (_u64, []),
     "golp_last_transfer": (_int, [C.POINTER(_u64), C.POINTER(_u64)]),
@@ -86,6 +91,7 @@ SIGNATURES = {
     "golp_host_free": (_int, [_vp, _u64]),
     "golp_host_register": (_int, [_vp, _u64]),
     "golp_host_is_pinned": (_int, [_vp]),
+    "golp_host_is_pinned_range": (_int, [_vp, _u64]),
     "golp_host_unregister": (_int, [_vp]),
     "golp_host_topk": (_int, [_vp, _vp, _u64, _u64, _vp, _int]),
     "golp_host_hash_build": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),

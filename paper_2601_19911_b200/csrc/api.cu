@@ -12,9 +12,12 @@
 #include <unistd.h>
 
 #include <map>
+#include <set>
+#include <string>
 
 #include "../../include/golp_b200.h"
 #include "join.cuh"
+#include "probe.cuh"
 #include "runtime.h"
 #include "sort.cuh"
 #include "topk.cuh"
@@ -114,6 +117,8 @@ struct Ctx {
   DevBuf sc_prow, sc_off, sc_cnt;
   DevBuf part_keys, part_pos, part_cnt, part_cur, run_base, run_len, res_part, work_ctr;
   DevBuf pairs_p, pairs_b;
+  DevBuf fstat;             // direct probe: ticket, staging bump, per-tile counts / staged offsets
+  DevBuf stage_p, stage_b;  // direct probe: pair staging area
   DevBuf rows_flag;  // build row column is a dense run (join_build_impl)
   DevBuf row_base;   // what the emit adds to a singleton's slot.off (rows[0] for a dense column, else 0)
   DevBuf srt_hist, srt_k0, srt_k1, srt_r0, srt_r1, srt_status, srt_base;
@@ -136,19 +141,84 @@ struct Ctx {
   bool topk_pending = false;  // fused Top-K in flight: candidates/fallback read on demand
   bool topk_timed = false;
   golp_kernel_times kt{};
+  // Per-context launch caches: kernels whose dynamic shared memory limit was
+  // raised on this device, and occupancy-derived grid sizes.
+  std::set<const void*> smem_set;
+  std::map<std::pair<const void*, int>, int> per_sm;
+  std::vector<cudaEvent_t> trace_ev;  // GOLP_TRACE upload markers (golp_probe)
 };
 
-Ctx g;
+// One context per (device, handle): streams, pinned staging rings, HBM
+// workspace and launch caches. A thread works on one context at a time
+// (golp_init / golp_use_device / golp_context_use select it); calls stay
+// externally synchronous per context, and threads on different contexts run
+// concurrently (B200Device(gpus=G) drives G of them from G host threads).
+constexpr int kMaxContexts = 64;
+std::mutex g_ctx_mu;
+Ctx* g_ctx[kMaxContexts] = {};
+int g_default_ctx[kMaxContexts];  // device -> handle of its default context (-1: none)
+bool g_default_init = false;
+thread_local Ctx* t_cur = nullptr;
+std::atomic<bool> g_any_ready{false};  // some context initialized the CUDA runtime
 
-int do_init(int device, uint64_t chunk_bytes, int host_threads) {
-  if (g.ready) return GOLP_OK;
+int device_of_thread() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) {
+    cudaGetLastError();
+    d = 0;
+  }
+  return d;
+}
+
+// Handle of the default context of `device`, created (not yet initialized) on first use.
+int default_handle(int device) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (!g_default_init) {
+    for (int& h : g_default_ctx) h = -1;
+    g_default_init = true;
+  }
+  if (device < 0 || device >= kMaxContexts) return -1;
+  if (g_default_ctx[device] >= 0) return g_default_ctx[device];
+  for (int h = 0; h < kMaxContexts; ++h)
+    if (!g_ctx[h]) {
+      g_ctx[h] = new Ctx();
+      g_ctx[h]->device = device;
+      g_default_ctx[device] = h;
+      return h;
+    }
+  return -1;
+}
+
+// The calling thread's context (the current CUDA device's default one when the
+// thread has not selected any); initialized by ensure_init().
+Ctx& cur() {
+  if (!t_cur) {
+    const int h = default_handle(device_of_thread());
+    t_cur = g_ctx[h >= 0 ? h : 0];
+  }
+  return *t_cur;
+}
+
+int do_init(Ctx& g, int device, uint64_t chunk_bytes, int host_threads) {
+  if (g.ready) {
+    if (device >= 0 && device != g.device) {
+      set_error("context is bound to device " + std::to_string(g.device) + ", not " + std::to_string(device));
+      return GOLP_ERR_INVALID;
+    }
+    CK(cudaSetDevice(g.device));
+    return GOLP_OK;
+  }
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (ndev <= 0) {
     set_error("no CUDA device visible");
     return GOLP_ERR_CUDA;
   }
-  if (device < 0) CK(cudaGetDevice(&device));
+  if (device < 0) device = g.device;
+  if (device < 0 || device >= ndev) {
+    set_error("CUDA device " + std::to_string(device) + " is not visible (" + std::to_string(ndev) + " devices)");
+    return GOLP_ERR_INVALID;
+  }
   CK(cudaSetDevice(device));
   g.device = device;
   CK(cudaDeviceGetAttribute(&g.sms, cudaDevAttrMultiProcessorCount, device));
@@ -174,12 +244,67 @@ int do_init(int device, uint64_t chunk_bytes, int host_threads) {
   if (const char* v = getenv("GOLP_DENSE_ROWS")) g.dense_rows = std::atoi(v) != 0;
   CK(g.ctl.ensure(sizeof(SelectCtl) * kNumCtl));
   g.ready = true;
+  g_any_ready = true;
   return GOLP_OK;
 }
 
-int ensure_init() { return g.ready ? GOLP_OK : do_init(-1, 0, 0); }
+// Initializes the calling thread's context on first use and makes its device
+// current on this thread.
+int ensure_init() {
+  Ctx& g = cur();
+  if (!g.ready) return do_init(g, -1, 0, 0);
+  int d = -1;
+  if (cudaGetDevice(&d) != cudaSuccess || d != g.device) CK(cudaSetDevice(g.device));
+  return GOLP_OK;
+}
 
-SelectCtl* ctl(int i) { return g.ctl.as<SelectCtl>() + i; }
+// A device pointer handed to a resident entry point must live on the context's
+// device (a tensor on another GPU would be a foreign pointer to this context).
+int check_device_ptr(const void* p) {
+  if (!p) return GOLP_OK;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return GOLP_OK;  // not a CUDA allocation the runtime knows: let the kernel fault report it
+  }
+  const int dev = cur().device;
+  if ((at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) && at.device != dev) {
+    set_error("device pointer is on CUDA device " + std::to_string(at.device) + " but the golp context is on " +
+              std::to_string(dev));
+    return GOLP_ERR_INVALID;
+  }
+  return GOLP_OK;
+}
+
+// Raises `fn`'s dynamic shared memory limit once per context (per device).
+template <typename K>
+int smem_attr(K fn, size_t smem) {
+  Ctx& g = cur();
+  const void* key = reinterpret_cast<const void*>(fn);
+  if (smem == 0 || g.smem_set.count(key)) return GOLP_OK;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  g.smem_set.insert(key);
+  return GOLP_OK;
+}
+
+// Resident blocks per SM of `fn` at (threads, smem), cached per context; 0 if it cannot run.
+template <typename K>
+int blocks_per_sm(K fn, int threads, size_t smem) {
+  Ctx& g = cur();
+  const auto key = std::make_pair(reinterpret_cast<const void*>(fn), threads * 1024 + (int)(smem >> 10));
+  auto it = g.per_sm.find(key);
+  if (it != g.per_sm.end()) return it->second;
+  if (smem_attr(fn, smem) != GOLP_OK) return 0;
+  int per = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    per = 0;
+  }
+  g.per_sm[key] = per;
+  return per;
+}
+
+SelectCtl* ctl(int i) { return cur().ctl.as<SelectCtl>() + i; }
 
 // Integer tuning knob from the environment (default when unset or malformed).
 uint64_t env_u64(const char* name, uint64_t dflt) {
@@ -190,25 +315,39 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
   return (end && *end == 0) ? (uint64_t)x : dflt;
 }
 
+// Page-locked host ranges this library knows about: the pinned result arena's
+// regions and the caller buffers golp_host_register page-locked. A transfer
+// takes the direct-DMA path only when its WHOLE range lies in one of them
+// (a registered prefix view says nothing about the bytes after it); any other
+// buffer goes through the staging ring.
+std::mutex g_pin_mu;
+std::map<uintptr_t, size_t> g_pinned;  // base -> bytes
 
-// True when `p` lies in page-locked host memory (cudaHostAlloc'd, our result
-// arena, or a cudaHostRegister'ed caller buffer): the DMA engine can use it directly.
-bool is_pinned(const void* p) {
+void pinned_add(const void* p, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pinned[reinterpret_cast<uintptr_t>(p)] = bytes;
+}
+void pinned_remove(const void* p) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pinned.erase(reinterpret_cast<uintptr_t>(p));
+}
+bool is_pinned(const void* p, size_t bytes) {
   if (!p) return false;
-  cudaPointerAttributes at;
-  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return at.type == cudaMemoryTypeHost;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  auto it = g_pinned.upper_bound(a);
+  if (it == g_pinned.begin()) return false;
+  --it;
+  return a >= it->first && a + std::max<size_t>(bytes, 1) <= it->first + it->second;
 }
 
 // ---- pinned staging ring ----------------------------------------------------------
 // Host -> device copy of an arbitrary pageable buffer: the pool packs chunk i+1
 // into a pinned slot while the DMA engine drains chunk i.
 int stage_h2d(void* dst, const void* src, size_t bytes) {
+  Ctx& g = cur();
   g.moved_h2d += bytes;
-  if (bytes && is_pinned(src)) {  // page-locked source: no host copy
+  if (bytes && is_pinned(src, bytes)) {  // page-locked source: no host copy
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g.s_h2d));
     return GOLP_OK;
   }
@@ -241,6 +380,7 @@ __global__ void fill_dense_rows_kernel(uint32_t* __restrict__ dst, uint32_t base
 // next upload until it finished). Any other column is copied as is. The
 // device therefore sees exactly the caller's row ids either way.
 int upload_rows(uint32_t* dst, const uint32_t* src, uint64_t n, bool* copied = nullptr) {
+  Ctx& g = cur();
   if (copied) *copied = false;
   if (!n) return GOLP_OK;
   const double tv = wall_seconds();
@@ -262,6 +402,7 @@ int upload_rows(uint32_t* dst, const uint32_t* src, uint64_t n, bool* copied = n
 // Full-row mode ships payload bytes the device never reads: stream a pinned slot
 // (contents irrelevant) into a device scratch chunk, repeatedly.
 int stage_dummy_h2d(size_t bytes) {
+  Ctx& g = cur();
   if (!bytes) return GOLP_OK;
   g.moved_h2d += bytes;
   CK(g.in_payload.ensure(g.chunk));
@@ -283,6 +424,7 @@ int stage_dummy_h2d(size_t bytes) {
 // pieces are DMA'd on s_d2h and unpacked (pool memcpy) in FIFO order, either
 // opportunistically (d2h_poll) or when a slot is needed / at the end (d2h_flush).
 int d2h_complete_one() {
+  Ctx& g = cur();
   Ctx::D2HPiece pc = g.d2h_q[g.d2h_head++];
   CK(cudaEventSynchronize(g.dpin_ev[pc.slot]));
   parallel_copy(g.pool, pc.dst, g.dpin[pc.slot], pc.len);
@@ -294,8 +436,9 @@ int d2h_complete_one() {
 }
 
 int d2h_enqueue(void* dst, const void* src, size_t bytes) {
+  Ctx& g = cur();
   g.moved_d2h += bytes;
-  if (bytes && is_pinned(dst)) {  // page-locked destination (result arena): no host copy
+  if (bytes && is_pinned(dst, bytes)) {  // page-locked destination (result arena): no host copy
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g.s_d2h));
     g.d2h_direct = true;
     return GOLP_OK;
@@ -314,6 +457,7 @@ int d2h_enqueue(void* dst, const void* src, size_t bytes) {
 }
 
 int d2h_poll() {
+  Ctx& g = cur();
   while (g.d2h_head < g.d2h_q.size()) {
     const cudaError_t e = cudaEventQuery(g.dpin_ev[g.d2h_q[g.d2h_head].slot]);
     if (e == cudaErrorNotReady) return GOLP_OK;
@@ -324,6 +468,7 @@ int d2h_poll() {
 }
 
 int d2h_flush() {
+  Ctx& g = cur();
   while (g.d2h_head < g.d2h_q.size()) RET(d2h_complete_one());
   if (g.d2h_direct) {
     CK(cudaStreamSynchronize(g.s_d2h));
@@ -338,6 +483,7 @@ int stage_d2h(void* dst, const void* src, size_t bytes) {
 }
 
 int sync_ring() {
+  Ctx& g = cur();
   for (int i = 0; i < kSlots; ++i) {
     if (g.pin_busy[i]) CK(cudaEventSynchronize(g.pin_ev[i]));
     g.pin_busy[i] = false;
@@ -346,6 +492,7 @@ int sync_ring() {
 }
 
 int ensure_chunk_events(size_t n) {
+  Ctx& g = cur();
   while (g.chunk_ev.size() < n) {
     cudaEvent_t e, f;
     CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -416,14 +563,16 @@ void* arena_alloc(size_t bytes) {
       }
     }
     const size_t want = std::max(kArenaRegion, len);
-    if (g_arena_total + want > arena_max() || !g.ready) return nullptr;
+    if (g_arena_total + want > arena_max() || !g_any_ready.load()) return nullptr;
     void* base = nullptr;
-    if (cudaHostAlloc(&base, want, cudaHostAllocDefault) != cudaSuccess) {
+    // portable: result arrays of every context (device) DMA straight into it
+    if (cudaHostAlloc(&base, want, cudaHostAllocPortable) != cudaSuccess) {
       cudaGetLastError();
       return nullptr;
     }
     ArenaRegion reg{static_cast<char*>(base), want, {}};
     reg.free_[0] = want;
+    pinned_add(base, want);
     g_arena.push_back(std::move(reg));
     g_arena_total += want;
   }
@@ -487,29 +636,21 @@ TopkPlan plan_topk(uint64_t n, uint64_t kk) {
 
 template <class Src>
 int launch_select(const SelectArgs<Src>& a, cudaStream_t s) {
-  static int blocks = 0;
+  Ctx& g = cur();
   const size_t smem = (size_t)kSortTile * (sizeof(uint64_t) + sizeof(uint32_t));
+  RET(smem_attr(select_kernel<Src>, smem));
   if (!a.use_cand_count && a.n <= kSortTile) {  // one block, shared memory only: plain launch
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(select_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
     select_kernel<Src><<<1, kSelThreads, smem, s>>>(a);
     CKL();
     ++g_launches;
     return GOLP_OK;
   }
-  if (!blocks) {
-    CK(cudaFuncSetAttribute(select_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, select_kernel<Src>, kSelThreads, smem));
-    if (per < 1) {
-      set_error("select_kernel cannot be co-resident");
-      return GOLP_ERR_CUDA;
-    }
-    blocks = per * g.sms;
+  const int per = blocks_per_sm(select_kernel<Src>, kSelThreads, smem);
+  if (per < 1) {
+    set_error("select_kernel cannot be co-resident");
+    return GOLP_ERR_CUDA;
   }
+  const int blocks = per * g.sms;
   void* args[] = {const_cast<SelectArgs<Src>*>(&a)};
   CK(cudaLaunchCooperativeKernel((const void*)select_kernel<Src>, dim3(blocks), dim3(kSelThreads), args, smem, s));
   ++g_launches;
@@ -519,6 +660,7 @@ int launch_select(const SelectArgs<Src>& a, cudaStream_t s) {
 template <class Src>
 SelectArgs<Src> make_args(Src src, uint64_t n, uint64_t need, int mode, int c, uint32_t* out_rows,
                           uint64_t* out_hi) {
+  Ctx& g = cur();
   SelectArgs<Src> a;
   a.src = src;
   a.n = n;
@@ -538,13 +680,9 @@ SelectArgs<Src> make_args(Src src, uint64_t n, uint64_t need, int mode, int c, u
 
 template <class Src>
 int launch_rank(const SelectArgs<Src>& a, unsigned long long* clear_count, cudaStream_t s) {
-  static int blocks = 0;
-  if (!blocks) {
-    CK(cudaFuncSetAttribute(rank_select_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRankSmem));
-    int per = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rank_select_kernel<Src>, kRankThreads, kRankSmem));
-    blocks = std::max(1, per) * g.sms;
-  }
+  Ctx& g = cur();
+  RET(smem_attr(rank_select_kernel<Src>, kRankSmem));
+  const int blocks = std::max(1, blocks_per_sm(rank_select_kernel<Src>, kRankThreads, kRankSmem)) * g.sms;
   rank_select_kernel<Src><<<blocks, kRankThreads, kRankSmem, s>>>(a, clear_count);
   CKL();
   ++g_launches;
@@ -552,6 +690,7 @@ int launch_rank(const SelectArgs<Src>& a, unsigned long long* clear_count, cudaS
 }
 
 int ensure_topk_ws(uint64_t kk, uint64_t cap) {
+  Ctx& g = cur();
   CK(g.w_hi.ensure(std::max<uint64_t>(kk, 1) * 16));  // winners + merge buffer
   CK(g.w_lo.ensure(std::max<uint64_t>(kk, 1) * 8));
   if (cap) {
@@ -562,6 +701,7 @@ int ensure_topk_ws(uint64_t kk, uint64_t cap) {
 }
 
 int launch_filter(const double* keys, const uint32_t* rows, uint64_t n, uint64_t cap, cudaStream_t s) {
+  Ctx& g = cur();
   if (n == 0) return GOLP_OK;
   const uint64_t vec = n / 2 + 1;
   uint64_t blocks = (vec + (uint64_t)kFilterThreads * kFilterUnroll - 1) / ((uint64_t)kFilterThreads * kFilterUnroll);
@@ -575,6 +715,7 @@ int launch_filter(const double* keys, const uint32_t* rows, uint64_t n, uint64_t
 }
 
 void prof_record(int idx, cudaStream_t s) {
+  Ctx& g = cur();
   if (!g.prof) return;
   // Inside a CUDA-graph capture the record must be an external event node, or
   // the event cannot be synchronized / timed after a replay.
@@ -585,6 +726,7 @@ void prof_record(int idx, cudaStream_t s) {
     cudaEventRecord(g.ev[idx], s);
 }
 double prof_ms(int a, int b) {
+  Ctx& g = cur();
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, g.ev[a], g.ev[b]) != cudaSuccess) return 0.0;
   return (double)ms;
@@ -593,6 +735,7 @@ double prof_ms(int a, int b) {
 // Status / candidate count of a sampled run: the select kernel stores them into
 // mapped pinned words, so one stream sync replaces a D2H copy + sync.
 int ensure_status_words() {
+  Ctx& g = cur();
   if (!g.status_host) {
     CK(cudaHostAlloc(reinterpret_cast<void**>(&g.status_host), 64, cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g.status_dev), g.status_host, 0));
@@ -603,6 +746,7 @@ int ensure_status_words() {
 // status: 0 ok, 1 candidate set unusable (direct fallback), 2 too many
 // candidates for the rank kernel (grid engine over the same candidates).
 int read_topk_status(cudaStream_t s, int* status, uint64_t* cands) {
+  Ctx& g = cur();
   CK(cudaStreamSynchronize(s));
   *status = *reinterpret_cast<volatile int*>(g.status_host);
   *cands = *reinterpret_cast<volatile unsigned long long*>(g.status_host + 8);
@@ -610,6 +754,7 @@ int read_topk_status(cudaStream_t s, int* status, uint64_t* cands) {
 }
 
 SelectArgs<SrcCand> cand_args(uint64_t kk, uint64_t cap, uint32_t* out_rows, uint64_t* out_hi) {
+  Ctx& g = cur();
   SelectArgs<SrcCand> a = make_args(SrcCand{g.cand_hi.as<uint64_t>(), g.cand_lo.as<uint32_t>()}, 0, kk, kModeFull, 1,
                                     out_rows, out_hi);
   a.use_cand_count = 1;
@@ -631,6 +776,7 @@ int topk_direct(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k
 // Top-K over device-resident columns (sampling on the device).
 int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, uint32_t* out_rows,
                      uint64_t* out_hi, cudaStream_t s) {
+  Ctx& g = cur();
   const uint64_t kk = std::min(k, n);
   if (kk == 0) return GOLP_OK;
   const TopkPlan p = plan_topk(n, kk);
@@ -675,20 +821,15 @@ int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint6
       f.out_hi = out_hi;
       f.host_count = reinterpret_cast<unsigned long long*>(g.status_dev + 8);
       f.host_status = reinterpret_cast<int*>(g.status_dev);
-      static int blocks = 0;
       const size_t smem = (size_t)kSortTile * (sizeof(uint64_t) + sizeof(uint32_t));
-      if (!blocks) {
-        CK(cudaFuncSetAttribute(topk_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int per = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, topk_fused_kernel, kSelThreads, smem));
-        if (per < 1) {
-          set_error("topk_fused_kernel cannot be co-resident");
-          return GOLP_ERR_CUDA;
-        }
-        // blocks per SM (test / tuning knob GOLP_TOPK_FUSED_PER_SM; default: all that fit)
-        per = (int)std::min<uint64_t>((uint64_t)per, std::max<uint64_t>(1, env_u64("GOLP_TOPK_FUSED_PER_SM", per)));
-        blocks = per * g.sms;
+      int per = blocks_per_sm(topk_fused_kernel, kSelThreads, smem);
+      if (per < 1) {
+        set_error("topk_fused_kernel cannot be co-resident");
+        return GOLP_ERR_CUDA;
       }
+      // blocks per SM (test / tuning knob GOLP_TOPK_FUSED_PER_SM; default: all that fit)
+      per = (int)std::min<uint64_t>((uint64_t)per, std::max<uint64_t>(1, env_u64("GOLP_TOPK_FUSED_PER_SM", per)));
+      const int blocks = per * g.sms;
       CK(cudaMemsetAsync(ctl(1), 0, 2 * sizeof(SelectCtl), s));  // candidate + fallback controls
       void* args[] = {&f};
       CK(cudaLaunchCooperativeKernel((void*)topk_fused_kernel, blocks, kSelThreads, args, smem, s));
@@ -746,6 +887,7 @@ int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint6
 
 // ---- join -------------------------------------------------------------------------
 int grid_for(uint64_t n, int threads, int per_sm) {
+  Ctx& g = cur();
   uint64_t b = (n + threads - 1) / threads;
   b = std::max<uint64_t>(1, std::min<uint64_t>(b, (uint64_t)g.sms * per_sm));
   return (int)b;
@@ -756,6 +898,7 @@ int grid_for(uint64_t n, int threads, int per_sm) {
 // kMaxProbeParts slices.
 
 void plan_partitions(uint64_t cap) {
+  Ctx& g = cur();
   const uint64_t slice_bytes = std::max<uint64_t>(64, env_u64("GOLP_JOIN_SLICE_BYTES", 32ull << 20));
   uint64_t parts = 1;
   if (cap * sizeof(Slot) > 2 * slice_bytes) {
@@ -775,15 +918,13 @@ void plan_partitions(uint64_t cap) {
 // (a queued block would start its walk far behind the others).
 template <typename K>
 int resident_grid(K kernel, int threads, size_t smem) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
-    per_sm = 1;
-  return per_sm * g.sms;
+  return std::max(1, blocks_per_sm(kernel, threads, smem)) * cur().sms;
 }
 
 // Groups the entries of [keys, keys+n) by table slice into g.part_keys, with
 // positions (build) or in-tile indices + (tile, slice) runs (probe). 3 launches.
 int partition_entries(const double* keys, uint64_t n, bool probe_side, cudaStream_t s) {
+  Ctx& g = cur();
   const uint32_t P = g.jparts;
   const uint64_t ntiles = (n + kPartTile - 1) / kPartTile;
   CK(g.part_keys.ensure(std::max<uint64_t>(n, 1) * 8));
@@ -801,20 +942,16 @@ int partition_entries(const double* keys, uint64_t n, bool probe_side, cudaStrea
     o.pos = g.part_pos.as<uint32_t>();
   }
   unsigned long long* cnt = g.part_cnt.as<unsigned long long>();
-  unsigned long long* cur = g.part_cur.as<unsigned long long>();
+  unsigned long long* cursors = g.part_cur.as<unsigned long long>();
   CK(cudaMemsetAsync(cnt, 0, P * 8, s));
   part_count_kernel<<<g.sms * 4, kPartThreads, 0, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cnt);
   CKL();
-  part_scan_kernel<<<1, 1024, 0, s>>>(cnt, cur, P);
+  part_scan_kernel<<<1, 1024, 0, s>>>(cnt, cursors, P);
   CKL();
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(part_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartScatterSmem));
-    attr = true;
-  }
-  static const int gsmax = resident_grid(part_scatter_kernel, kPartThreads, kPartScatterSmem);
+  RET(smem_attr(part_scatter_kernel, kPartScatterSmem));
+  const int gsmax = resident_grid(part_scatter_kernel, kPartThreads, kPartScatterSmem);
   const int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)gsmax));
-  part_scatter_kernel<<<gs, kPartThreads, kPartScatterSmem, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cur, o);
+  part_scatter_kernel<<<gs, kPartThreads, kPartScatterSmem, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cursors, o);
   CKL();
   g_launches += 3;
   return GOLP_OK;
@@ -823,10 +960,11 @@ int partition_entries(const double* keys, uint64_t n, bool probe_side, cudaStrea
 // Slice-ordered lookups of [pkeys, pkeys+n): partition by table slice, then
 // g.res_part[i] = packed slot of g.part_keys[i] (4 launches).
 int probe_partitioned(const double* pkeys, uint64_t n, cudaStream_t s) {
+  Ctx& g = cur();
   RET(partition_entries(pkeys, n, true, s));
   CK(g.res_part.ensure(n * 8));
-  static const int grid = resident_grid(join_probe_part_kernel, kProbeThreads, 0);
-  static const int policy = (int)env_u64("GOLP_JOIN_PART_POLICY", 0);
+  const int grid = resident_grid(join_probe_part_kernel, kProbeThreads, 0);
+  const int policy = (int)env_u64("GOLP_JOIN_PART_POLICY", 0);
   const uint64_t items = (uint64_t)kProbeThreads * kPartProbeItems;
   const int gp = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + items - 1) / items, (uint64_t)grid));
   CK(g.work_ctr.ensure(8));
@@ -847,6 +985,7 @@ int probe_partitioned(const double* pkeys, uint64_t n, cudaStream_t s) {
 constexpr uint64_t kDenseCheckMin = 256u << 10;
 
 int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cudaStream_t s, int rows_dense = 0) {
+  Ctx& g = cur();
   uint64_t cap = 1024;
   while (cap < 2 * nb && cap < (1ull << 32)) cap <<= 1;
   if (cap < 2 * nb || cap * kInline + nb > (1ull << 32)) {
@@ -903,7 +1042,7 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   int gb = grid_for((nb + kBuildItems - 1) / kBuildItems, kBuildThreads, 8);
   TileSched sched{nullptr};
   if (ipos) {  // partitioned order: blocks claim tiles in order (see TileSched)
-    static const int grid = resident_grid(join_insert_kernel<true>, kBuildThreads, 0);
+    const int grid = resident_grid(join_insert_kernel<true>, kBuildThreads, 0);
     gb = std::min(gb, grid);
     CK(g.work_ctr.ensure(8));
     CK(cudaMemsetAsync(g.work_ctr.p, 0, 8, s));
@@ -924,12 +1063,8 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   CKL();
   join_group_sort_kernel<<<g.sms, 256, 0, s>>>(table, ga, br);
   CKL();
-  static bool attr = false;
   const size_t smem = kGroupTile * sizeof(uint32_t);
-  if (!attr) {
-    CK(cudaFuncSetAttribute(join_big_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  RET(smem_attr(join_big_groups_kernel, smem));
   join_big_groups_kernel<<<std::max(1, g.sms / 4), 1024, smem, s>>>(table, ga, br);
   CKL();
   g_launches += 5;
@@ -937,29 +1072,69 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   return GOLP_OK;
 }
 
-// One probe over [pkeys, pkeys+np): match -> scan of block totals -> emit, per
-// sub-chunk (the sub-chunk bounds the scratch). Pair offsets continue from
-// *base_in; *total_out = *base_in + pairs of this call.
+// Direct probe of [pkeys, pkeys+np) (probe.cuh): warp tiles look up and stage
+// their pairs (one launch), tile counts are scanned into output offsets chained
+// after *base_in, the staged runs are placed. *total_out = *base_in + pairs.
+// Pairs at positions >= cap are counted, not written.
+int launch_probe_direct(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
+                        uint64_t cap, const unsigned long long* base_in, unsigned long long* total_out,
+                        cudaStream_t s) {
+  Ctx& g = cur();
+  const uint64_t ntiles = (np + kPSpan - 1) / kPSpan;
+  const uint64_t nplace = (ntiles + kPlaceTiles - 1) / kPlaceTiles;
+  CK(g.fstat.ensure((2 + nplace + 2 * ntiles) * 8));
+  // [0] ticket, [1] staging bump, [2, 2+nplace) placement look-back words, then per tile
+  unsigned long long* ctr = g.fstat.as<unsigned long long>();
+  unsigned long long* place_status = ctr + 2;
+  unsigned long long* tile_count = place_status + nplace;
+  unsigned long long* tile_stage = tile_count + ntiles;
+  CK(cudaMemsetAsync(ctr, 0, (2 + nplace) * 8, s));
+  const uint64_t stage_cap = std::max<uint64_t>(cap, 1);
+  CK(g.stage_p.ensure(stage_cap * 4));
+  CK(g.stage_b.ensure(stage_cap * 4));
+  const int per = blocks_per_sm(join_probe_lookup_kernel, kPThreads, kPSmem);
+  if (per < 1) {
+    set_error("join_probe_lookup_kernel cannot be resident");
+    return GOLP_ERR_CUDA;
+  }
+  const uint64_t grid = std::min<uint64_t>((ntiles + kPWarps - 1) / kPWarps, (uint64_t)per * g.sms);
+  ProbeLookupArgs a;
+  a.keys = pkeys;
+  a.rows = prows;
+  a.np = np;
+  a.table = g.table.as<Slot>();
+  a.mask = (uint32_t)g.jmask;
+  a.csr_row = g.rows_arr.as<uint32_t>();
+  a.row_base = g.row_base.as<uint32_t>();
+  a.stage_p = g.stage_p.as<uint32_t>();
+  a.stage_b = g.stage_b.as<uint32_t>();
+  a.stage_cap = stage_cap;
+  a.ticket = ctr;
+  a.bump = ctr + 1;
+  a.tile_count = tile_count;
+  a.tile_stage = tile_stage;
+  join_probe_lookup_kernel<<<(unsigned)grid, kPThreads, kPSmem, s>>>(a);
+  CKL();
+  join_probe_place_kernel<<<(unsigned)nplace, kPlaceThreads, 0, s>>>(a.stage_p, a.stage_b, stage_cap, tile_count,
+                                                                  tile_stage, ntiles, place_status, base_in,
+                                                                  total_out, out_p, out_b, cap);
+  CKL();
+  g_launches += 2;
+  return GOLP_OK;
+}
+
+// One probe over [pkeys, pkeys+np). Tables probed directly: launch_probe_direct.
+// Radix-partitioned probes (C4-sized tables): per span, partition + slice-
+// ordered lookups, then match -> scan of block totals -> emit per sub-chunk
+// (the sub-chunk bounds the scratch). Pair offsets continue from *base_in;
+// *total_out = *base_in + pairs of this call.
 int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
                  uint64_t cap, const unsigned long long* base_in, unsigned long long* total_out, cudaStream_t s) {
+  Ctx& g = cur();
   if (np == 0 || g.jnb == 0) {
     CK(cudaMemcpyAsync(total_out, base_in, 8, cudaMemcpyDeviceToDevice, s));
     return GOLP_OK;
   }
-  constexpr uint64_t kSub = 1ull << 27;  // probes per sub-chunk (scratch <= 1.5 GiB)
-  const uint64_t sub = std::min(np, kSub);
-  const uint64_t nwt_max = (sub + kWarpTile - 1) / kWarpTile;
-  const uint64_t nwarps_max = (uint64_t)g.sms * GOLP_PROBE_MINB * kProbeWarps;
-  CK(g.sc_prow.ensure(nwt_max * kWarpTile * 4));
-  CK(g.sc_off.ensure(nwt_max * kWarpTile * 4));
-  CK(g.sc_cnt.ensure(nwt_max * kWarpTile * 4));
-  CK(g.wcount.ensure(std::max(nwt_max, nwarps_max) * 8));
-  CK(g.totals2.ensure(16));
-  MatchScratch sc;
-  sc.prow = g.sc_prow.as<uint32_t>();
-  sc.off = g.sc_off.as<uint32_t>();
-  sc.cnt = g.sc_cnt.as<uint32_t>();
-  unsigned long long* tmp = g.totals2.as<unsigned long long>();
   // Partition the probe side (in spans of kSpan probes) when a span reuses each
   // table slice several times: span * 32 B of slot-pair reads >= 2x the table.
   // (GOLP_JOIN_SPAN shrinks the span so tests cover several spans on small inputs.)
@@ -967,6 +1142,22 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
   const uint64_t force = env_u64("GOLP_JOIN_PART_PROBE", 2);
   const bool part_probe =
       g.jparts > 1 && (force == 1 || (force == 2 && std::min(np, kSpan) >= g.jcap));
+  if (!part_probe && env_u64("GOLP_JOIN_DIRECT", 1))
+    return launch_probe_direct(pkeys, prows, np, out_p, out_b, cap, base_in, total_out, s);
+  constexpr uint64_t kSub = 1ull << 27;  // probes per sub-chunk (scratch <= 1.5 GiB)
+  const uint64_t sub = std::min(np, kSub);
+  const uint64_t nwt_max = (sub + kWarpTile - 1) / kWarpTile;
+  const uint64_t nwarps_max = (uint64_t)g.sms * GOLP_PROBE_MINB * kProbeWarps;
+  CK(g.sc_prow.ensure(nwt_max * kWarpTile * 4));
+  CK(g.sc_off.ensure(nwt_max * kWarpTile * 4));
+  CK(g.sc_cnt.ensure(nwt_max * kWarpTile * 4));
+  CK(g.wcount.ensure((std::max(nwt_max, nwarps_max) + kProbeWarps) * 12));
+  CK(g.totals2.ensure(16));
+  MatchScratch sc;
+  sc.prow = g.sc_prow.as<uint32_t>();
+  sc.off = g.sc_off.as<uint32_t>();
+  sc.cnt = g.sc_cnt.as<uint32_t>();
+  unsigned long long* tmp = g.totals2.as<unsigned long long>();
   const uint64_t span = part_probe ? kSpan : np;
   uint64_t ci = 0;  // running sub-chunk index (pair-offset chaining)
   for (uint64_t s0 = 0; s0 < np; s0 += span) {
@@ -981,17 +1172,13 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
       const uint64_t per_warp = part_probe ? kRunWarpTiles : (nwt + want_warps - 1) / want_warps;
       const uint64_t warps = (nwt + per_warp - 1) / per_warp;
       const uint64_t blocks = (warps + kProbeWarps - 1) / kProbeWarps;
-      sc.wentries = g.wcount.as<uint32_t>();
-      sc.wpairs = sc.wentries + blocks * kProbeWarps;
+      sc.wpairs = g.wcount.as<unsigned long long>();
+      sc.wentries = reinterpret_cast<uint32_t*>(sc.wpairs + blocks * kProbeWarps);
       CK(g.partial.ensure(blocks * 8));
       unsigned long long* part = g.partial.as<unsigned long long>();
       if (part_probe) {
         const uint64_t tile0 = (c0 - s0) / kPartTile;  // sub-chunks start on partition tiles
-        static bool attr = false;
-        if (!attr) {
-          CK(cudaFuncSetAttribute(join_match_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunSmem));
-          attr = true;
-        }
+        RET(smem_attr(join_match_runs_kernel, kRunSmem));
         join_match_runs_kernel<<<(unsigned)blocks, kProbeThreads, kRunSmem, s>>>(
             prows + c0, cn, g.res_part.as<uint64_t>(), g.part_pos.as<uint16_t>(),
             g.run_base.as<uint32_t>() + tile0 * g.jparts, g.run_len.as<uint16_t>() + tile0 * g.jparts, g.jparts, sc,
@@ -1025,6 +1212,7 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
 }
 
 int read_u64(const void* dptr, uint64_t* out, cudaStream_t s) {
+  Ctx& g = cur();
   uint64_t* h = static_cast<uint64_t*>(g.pin_small);
   CK(cudaMemcpyAsync(h, dptr, 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -1037,6 +1225,7 @@ int read_probe_total(const void* dptr, uint64_t* out, cudaStream_t s) { return r
 
 int join_probe_impl(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
                     uint64_t cap, uint64_t* out_m, cudaStream_t s) {
+  Ctx& g = cur();
   CK(g.totals.ensure(16));
   unsigned long long* totals = g.totals.as<unsigned long long>();
   CK(cudaMemsetAsync(totals, 0, 16, s));
@@ -1070,6 +1259,7 @@ int check_mode(int mode, uint32_t payload_bytes, uint64_t* entry) {
 // single-bucket digits), then one onesweep pass per digit. The last pass writes
 // only the rows, straight into out_rows.
 int full_sort_impl(const double* keys, const uint32_t* rows, uint64_t n, uint32_t* out_rows, cudaStream_t s) {
+  Ctx& g = cur();
   g.kt.full_sort_passes = 0;
   if (n == 0) return GOLP_OK;
   prof_record(0, s);
@@ -1119,11 +1309,7 @@ int full_sort_impl(const double* keys, const uint32_t* rows, uint64_t n, uint32_
     CK(g.srt_k1.ensure(n * 8));
     CK(g.srt_r1.ensure(n * 4));
   }
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(sort_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem));
-    attr = true;
-  }
+  RET(smem_attr(sort_pass_kernel, kSortSmem));
   unsigned long long* status = g.srt_status.as<unsigned long long>();
   unsigned long long* ctr = status + ntiles * 256;
   const uint64_t* in_k = nullptr;
@@ -1155,23 +1341,16 @@ int full_sort_impl(const double* keys, const uint32_t* rows, uint64_t n, uint32_
 }
 }  // namespace
 
-// =====================================================================================
-extern "C" {
-
-const char* golp_last_error(void) { return last_error_cstr(); }
-int golp_version(void) { return 1; }
-
-int golp_init(int device, uint64_t pinned_chunk_bytes, int host_threads) {
-  return do_init(device, pinned_chunk_bytes, host_threads);
-}
-
-int golp_shutdown(void) {
-  if (!g.ready) return GOLP_OK;
-  cudaDeviceSynchronize();
+// Frees a context's streams, pinned staging and HBM workspace (the pinned
+// result arena outlives it: result arrays may still be alive).
+void release_context(Ctx& g) {
+  if (!g.ready) return;
+  cudaSetDevice(g.device);
+  for (cudaStream_t st : {g.s_main, g.s_h2d, g.s_d2h}) cudaStreamSynchronize(st);
   g.pool.stop();
   DevBuf* bufs[] = {&g.ctl, &g.cand_hi, &g.cand_lo, &g.w_hi, &g.w_lo, &g.out_rows, &g.out_hi, &g.samples,
                     &g.table, &g.rows_arr, &g.ovf, &g.big_list, &g.jcount,
-                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.srt_hist, &g.srt_k0, &g.srt_k1, &g.srt_r0, &g.srt_r1, &g.srt_status, &g.srt_base, &g.in_keys, &g.in_rows,
+                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.fstat, &g.stage_p, &g.stage_b, &g.srt_hist, &g.srt_k0, &g.srt_k1, &g.srt_r0, &g.srt_r1, &g.srt_status, &g.srt_base, &g.in_keys, &g.in_rows,
                     &g.in_bkeys, &g.in_brows, &g.in_payload, &g.rows_flag, &g.row_base};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < kSlots; ++i) {
@@ -1202,7 +1381,6 @@ int golp_shutdown(void) {
   g.mirror = nullptr;
   g.mirror_dev = nullptr;
   g.mirror_n = 0;
-  // the pinned result arena outlives shutdown: result arrays may still be alive
   for (auto& e : g.ev) {
     if (e) cudaEventDestroy(e);
     e = nullptr;
@@ -1214,19 +1392,88 @@ int golp_shutdown(void) {
   cudaStreamDestroy(g.s_d2h);
   g.jcap = g.jmask = g.jnb = 0;
   g.last_probe_valid = false;
+  g.smem_set.clear();
+  g.per_sm.clear();
+  for (cudaEvent_t e : g.trace_ev) cudaEventDestroy(e);
+  g.trace_ev.clear();
   g.ready = false;
+}
+
+// =====================================================================================
+extern "C" {
+
+const char* golp_last_error(void) { return last_error_cstr(); }
+int golp_version(void) { return 1; }
+
+int golp_init(int device, uint64_t pinned_chunk_bytes, int host_threads) {
+  if (device < 0) device = device_of_thread();
+  const int h = default_handle(device);
+  if (h < 0) return invalid("device index out of range");
+  t_cur = g_ctx[h];
+  return do_init(*t_cur, device, pinned_chunk_bytes, host_threads);
+}
+
+int golp_use_device(int device) { return golp_init(device, 0, 0); }
+
+int golp_current_device(int* device) {
+  if (!device) return invalid("null output");
+  RET(ensure_init());
+  *device = cur().device;
+  return GOLP_OK;
+}
+
+int golp_context_open(int device, uint64_t pinned_chunk_bytes, int host_threads, int* handle) {
+  if (!handle) return invalid("null handle");
+  if (device < 0) device = device_of_thread();
+  int h = -1;
+  {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    for (int i = 0; i < kMaxContexts; ++i)
+      if (!g_ctx[i]) {
+        g_ctx[i] = new Ctx();
+        g_ctx[i]->device = device;
+        h = i;
+        break;
+      }
+  }
+  if (h < 0) return invalid("too many golp contexts");
+  t_cur = g_ctx[h];
+  RET(do_init(*t_cur, device, pinned_chunk_bytes, host_threads));
+  *handle = h;
+  return GOLP_OK;
+}
+
+int golp_context_use(int handle) {
+  if (handle < 0 || handle >= kMaxContexts || !g_ctx[handle]) return invalid("unknown golp context");
+  t_cur = g_ctx[handle];
+  return ensure_init();
+}
+
+int golp_context_close(int handle) {
+  if (handle < 0 || handle >= kMaxContexts || !g_ctx[handle]) return invalid("unknown golp context");
+  release_context(*g_ctx[handle]);
+  return GOLP_OK;
+}
+
+// Releases every context (process-wide). Context objects stay allocated, so a
+// thread that still has one selected re-initializes it on its next call.
+int golp_shutdown(void) {
+  for (int h = 0; h < kMaxContexts; ++h)
+    if (g_ctx[h]) release_context(*g_ctx[h]);
   return GOLP_OK;
 }
 
 uint64_t golp_launch_count(void) { return g_launches.load(); }
 
 int golp_set_dense_rows(int on) {
+  Ctx& g = cur();
   RET(ensure_init());
   g.dense_rows = on != 0;
   return GOLP_OK;
 }
 
 int golp_last_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
+  Ctx& g = cur();
   if (!h2d_bytes || !d2h_bytes) return invalid("null output pointer");
   *h2d_bytes = g.moved_h2d;
   *d2h_bytes = g.moved_d2h;
@@ -1234,6 +1481,7 @@ int golp_last_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
 }
 
 int golp_set_profiling(int on) {
+  Ctx& g = cur();
   RET(ensure_init());
   g.prof = on != 0;
   g.build_timed = g.probe_timed = g.topk_timed = false;
@@ -1243,6 +1491,7 @@ int golp_set_profiling(int on) {
 // The timing flags stay set while profiling is on, so a CUDA graph that captured
 // the event records can be replayed and read again after every replay.
 int golp_last_kernel_times(golp_kernel_times* out) {
+  Ctx& g = cur();
   if (!out) return invalid("null output");
   if (g.topk_pending) {
     CK(cudaDeviceSynchronize());
@@ -1271,13 +1520,16 @@ int golp_topk_device(const double* d_keys, const uint32_t* d_rows, uint64_t n, u
   if (k < 1) return invalid("k must be at least 1");
   RET(ensure_init());
   if (n > 0 && (!d_keys || !d_rows || !d_out_rows)) return invalid("null device pointer");
+  RET(check_device_ptr(d_keys));
   return topk_device_impl(d_keys, d_rows, n, k, d_out_rows, d_out_keys, as_stream(stream));
 }
 
 int golp_full_sort_device(const double* d_keys, const uint32_t* d_rows, uint64_t n, uint32_t* d_out_rows,
                           void* stream) {
+  Ctx& g = cur();
   RET(ensure_init());
   if (n > 0 && (!d_keys || !d_rows || !d_out_rows)) return invalid("null device pointer");
+  RET(check_device_ptr(d_keys));
   cudaStream_t s = as_stream(stream);
   RET(full_sort_impl(d_keys, d_rows, n, d_out_rows, s));
   if (g.prof) {
@@ -1289,6 +1541,7 @@ int golp_full_sort_device(const double* d_keys, const uint32_t* d_rows, uint64_t
 
 int golp_full_sort(const double* keys, const uint32_t* rows, uint64_t n, int mode, uint32_t payload_bytes,
                    uint32_t* out_rows, golp_ledger* led) {
+  Ctx& g = cur();
   uint64_t entry = 0;
   RET(check_mode(mode, payload_bytes, &entry));
   if (!led) return invalid("null ledger");
@@ -1316,7 +1569,7 @@ int golp_full_sort(const double* keys, const uint32_t* rows, uint64_t n, int mod
   CK(cudaStreamSynchronize(s));
   if (g.prof) g.kt.full_sort_ms = prof_ms(0, 1);
   const double t2 = wall_seconds();
-  if (is_pinned(out_rows)) {
+  if (is_pinned(out_rows, n * 4)) {
     CK(cudaMemcpyAsync(out_rows, g.out_rows.p, n * 4, cudaMemcpyDeviceToHost, g.s_d2h));
     g.moved_d2h += n * 4;
     CK(cudaStreamSynchronize(g.s_d2h));
@@ -1335,6 +1588,7 @@ int golp_topk_merge_device(const uint64_t* d_key_codes, const uint32_t* d_rows, 
   RET(ensure_init());
   const uint64_t kk = std::min(k, n);
   if (kk == 0) return GOLP_OK;
+  RET(check_device_ptr(d_key_codes));
   cudaStream_t s = as_stream(stream);
   RET(ensure_topk_ws(kk, 0));
   CK(cudaMemsetAsync(ctl(2), 0, sizeof(SelectCtl), s));
@@ -1344,7 +1598,9 @@ int golp_topk_merge_device(const uint64_t* d_key_codes, const uint32_t* d_rows, 
 }
 
 int golp_join_build_device(const double* d_build_keys, const uint32_t* d_build_rows, uint64_t nb, void* stream) {
+  Ctx& g = cur();
   RET(ensure_init());
+  RET(check_device_ptr(d_build_keys));
   cudaStream_t s = as_stream(stream);
   RET(join_build_impl(d_build_keys, d_build_rows, nb, s));
   g.build_timed = g.prof;  // resolved lazily by golp_last_kernel_times (no sync here)
@@ -1354,8 +1610,10 @@ int golp_join_build_device(const double* d_build_keys, const uint32_t* d_build_r
 int golp_join_probe_device_async(const double* d_probe_keys, const uint32_t* d_probe_rows, uint64_t np,
                                  uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
                                  uint64_t* d_out_matches, void* stream) {
+  Ctx& g = cur();
   RET(ensure_init());
   if (!d_out_matches) return invalid("null d_out_matches");
+  RET(check_device_ptr(d_probe_keys));
   cudaStream_t s = as_stream(stream);
   CK(g.totals.ensure(16));
   unsigned long long* totals = g.totals.as<unsigned long long>();
@@ -1373,6 +1631,7 @@ int golp_join_probe_device(const double* d_probe_keys, const uint32_t* d_probe_r
                            uint64_t* out_matches, void* stream) {
   RET(ensure_init());
   if (!out_matches) return invalid("null out_matches");
+  RET(check_device_ptr(d_probe_keys));
   cudaStream_t s = as_stream(stream);
   RET(join_probe_impl(d_probe_keys, d_probe_rows, np, d_out_probe_rows, d_out_build_rows, cap, out_matches, s));
   if (*out_matches > cap) {
@@ -1385,6 +1644,7 @@ int golp_join_probe_device(const double* d_probe_keys, const uint32_t* d_probe_r
 // ---- host buffers (E2E) -----------------------------------------------------------------
 int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, int mode, uint32_t payload_bytes,
               uint32_t* out_rows, uint64_t* out_len, golp_ledger* led) {
+  Ctx& g = cur();
   if (k < 1) return invalid("k must be at least 1");
   uint64_t entry = 0;
   RET(check_mode(mode, payload_bytes, &entry));
@@ -1431,10 +1691,14 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     CK(cudaStreamSynchronize(s));  // the fused path is stream-ordered: charge its time to t_kernel
     const double t2 = wall_seconds();
     uint32_t* hbuf = static_cast<uint32_t*>(g.pin_small);
-    CK(cudaMemcpyAsync(hbuf, d_out, kk * 4, cudaMemcpyDeviceToHost, s));
-    g.moved_d2h += kk * 4;
-    CK(cudaStreamSynchronize(s));
-    std::memcpy(out_rows, hbuf, kk * 4);
+    if (kk * 4 <= g.pin_small_bytes) {
+      CK(cudaMemcpyAsync(hbuf, d_out, kk * 4, cudaMemcpyDeviceToHost, s));
+      g.moved_d2h += kk * 4;
+      CK(cudaStreamSynchronize(s));
+      std::memcpy(out_rows, hbuf, kk * 4);
+    } else {
+      RET(stage_d2h(out_rows, d_out, kk * 4));
+    }
     led->t_h2d = t1 - t0;
     led->t_kernel = t2 - t1;
     led->t_d2h = wall_seconds() - t2;
@@ -1536,6 +1800,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
 int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb, const double* probe_keys,
                const uint32_t* probe_rows, uint64_t np, int mode, uint32_t payload_bytes, uint32_t* out_probe_rows,
                uint32_t* out_build_rows, uint64_t out_cap, uint64_t* out_matches, golp_ledger* led) {
+  Ctx& g = cur();
   uint64_t entry = 0;
   RET(check_mode(mode, payload_bytes, &entry));
   if (!out_matches || !led) return invalid("null output pointer");
@@ -1559,7 +1824,7 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
 
   // GOLP_TRACE: per-upload host queue times and device completion times
   const bool trace = std::getenv("GOLP_TRACE") != nullptr;
-  static std::vector<cudaEvent_t> tr_ev;
+  std::vector<cudaEvent_t>& tr_ev = g.trace_ev;
   std::vector<double> tr_q;
   auto tr_mark = [&]() -> int {
     if (!trace) return GOLP_OK;
@@ -1609,7 +1874,8 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   // (A zero-copy variant -- the emit kernel storing pairs into the pinned arena
   // over PCIe -- measured 3x slower at C2: 4-byte scattered stores make poor
   // PCIe transactions.)
-  uint64_t dcap = std::max<uint64_t>(g.pairs_p.bytes / 4, std::max<uint64_t>(np, 1024));
+  // At least the caller's capacity: M > dcap then implies M > out_cap (copy_out path).
+  uint64_t dcap = std::max<uint64_t>(g.pairs_p.bytes / 4, std::max<uint64_t>(std::max<uint64_t>(np, out_cap), 1024));
   CK(g.pairs_p.ensure(dcap * 4));
   CK(g.pairs_b.ensure(dcap * 4));
   dcap = std::min(g.pairs_p.bytes, g.pairs_b.bytes) / 4;
@@ -1769,11 +2035,20 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   *out_matches = m;
   g.last_m = m;
   g.last_probe_valid = true;  // copy_out reads the device pair buffers
-  const bool delivered = streaming && m <= out_cap && streamed == nchunks;
+  bool delivered = streaming && m <= out_cap && streamed == nchunks;
+  if (!delivered && m <= out_cap) {
+    // Streaming stopped early (a re-probe into larger device buffers): the
+    // pairs still fit the caller's arrays, so deliver all of them here.
+    if (m) {
+      RET(stage_d2h(out_probe_rows, dev_p, m * 4));
+      RET(stage_d2h(out_build_rows, dev_b, m * 4));
+    }
+    delivered = true;
+  }
   led->t_h2d = t1 - t0;
   led->t_kernel = t2 - t1;
   if (delivered) {
-    led->t_d2h = t3 - t2;
+    led->t_d2h = wall_seconds() - t2;
     led->d2h_bytes = 8 * m;
   } else {
     led->t_kernel += t3 - t2;  // copy_out adds the D2H phase
@@ -1782,6 +2057,7 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
 }
 
 int golp_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m, golp_ledger* led) {
+  Ctx& g = cur();
   if (!g.last_probe_valid) return invalid("no probe result to copy out");
   if (m != g.last_m) return invalid("copy_out size does not match the last probe's match count");
   const double t0 = wall_seconds();
@@ -1818,7 +2094,8 @@ int golp_host_free(void* p, uint64_t bytes) {
   return munmap(p, bytes) == 0 ? GOLP_OK : GOLP_ERR_INVALID;
 }
 
-int golp_host_is_pinned(const void* p) { return is_pinned(p) ? 1 : 0; }
+int golp_host_is_pinned(const void* p) { return is_pinned(p, 1) ? 1 : 0; }
+int golp_host_is_pinned_range(const void* p, uint64_t bytes) { return is_pinned(p, bytes) ? 1 : 0; }
 
 // Page-lock a caller buffer in place (read-only) so repeated transfers of it skip
 // the staging copy. Slow (~5 GB/s): worth it only for buffers reused across calls.
@@ -1844,12 +2121,14 @@ int golp_host_register(const void* p, uint64_t bytes) {
                      (unsigned long long)bytes, (unsigned long long)(e - a), rc, rc ? errno : 0);
     }
   }
-  CK(cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterReadOnly));
+  CK(cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterReadOnly | cudaHostRegisterPortable));
+  pinned_add(p, bytes);
   return GOLP_OK;
 }
 
 int golp_host_unregister(const void* p) {
   if (!p) return GOLP_OK;
+  pinned_remove(p);
   CK(cudaHostUnregister(const_cast<void*>(p)));
   return GOLP_OK;
 }

@@ -70,6 +70,16 @@ __device__ __forceinline__ ulonglong2 cas128(void* addr, ulonglong2 cmp, ulonglo
 }
 
 constexpr uint32_t kInline = 4;
+
+// Home-pair overflow flag: bit 31 of the cnt word of a pair's FIRST slot is set
+// when some key whose home is that pair had to be stored further on (the pair
+// was full when it arrived). Keys are only ever inserted, so a probe whose key
+// is not in its home pair can stop there unless the flag is set: most misses
+// resolve in one lookup even when the home pair is full. Group sizes stay
+// below 2^30 (join_build_impl's capacity check), so the bit is free; every
+// reader of cnt masks it.
+constexpr uint32_t kOverflowBit = 1u << 31;
+constexpr uint32_t kCntMask = kOverflowBit - 1u;
 constexpr uint32_t kGroupTile = 16384;  // big groups up to this size sorted in shared memory (64 KB)
 
 __global__ void join_init_table_kernel(Slot* __restrict__ table, uint64_t cap) {
@@ -187,8 +197,13 @@ __global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double
       }
     }
 #pragma unroll
+    for (int j = 0; j < kBuildItems; ++j) {  // stored beyond its home pair: flag the home pair
+      const uint32_t hp = (uint32_t)home_slot(b[j], mask);
+      if (((valid >> j) & 1u) && (h[j] & ~1u) != hp) atomicOr(&table[hp].cnt, kOverflowBit);
+    }
+#pragma unroll
     for (int j = 0; j < kBuildItems; ++j)
-      if (dup & (1u << j)) r[j] = atomicAdd(&table[h[j]].cnt, 1u);
+      if (dup & (1u << j)) r[j] = atomicAdd(&table[h[j]].cnt, 1u) & kCntMask;
     if constexpr (!kWide) {
 #pragma unroll
       for (int j = 0; j < kBuildItems; ++j)
@@ -264,7 +279,7 @@ __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_
     if (h < cap) {
       const ulonglong2 sl = reinterpret_cast<const ulonglong2*>(table)[h];
       if (sl.x != kEmptyKey) {
-        cnt = (uint32_t)(sl.y >> 32);
+        cnt = (uint32_t)(sl.y >> 32) & kCntMask;
         first = (uint32_t)sl.y;
       }
     }
@@ -327,7 +342,7 @@ __global__ void join_group_sort_kernel(const Slot* __restrict__ table, GroupArra
   const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t gi = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gi < nbig; gi += wstride) {
     const uint32_t h = ga.big_list[gi];
-    const uint32_t cnt = table[h].cnt;
+    const uint32_t cnt = table[h].cnt & kCntMask;
     if (cnt > kThreadGroup) {
       if (lane == 0) ga.big_list[nbig + atomicAdd(&ga.counters[3], 1ull)] = h;  // block kernel's queue
       continue;
@@ -357,7 +372,7 @@ __global__ void __launch_bounds__(1024) join_big_groups_kernel(const Slot* __res
   const unsigned nhuge = (unsigned)*(volatile unsigned long long*)&ga.counters[3];
   for (unsigned gi = blockIdx.x; gi < nhuge; gi += gridDim.x) {
     const uint32_t h = ga.big_list[nbig + gi];
-    const uint32_t cnt = table[h].cnt;
+    const uint32_t cnt = table[h].cnt & kCntMask;
     uint32_t* seg = ga.rows + table[h].off;
     if (cnt <= kGroupTile) {
       for (uint32_t m = threadIdx.x; m < cnt; m += blockDim.x) s_pos[m] = seg[m];
@@ -731,11 +746,15 @@ __device__ __forceinline__ void st_hint(uint32_t* p, uint32_t v, uint64_t pol) {
 }
 
 // Checks one slot pair: 1 = found (off/cnt set), 0 = absent, -1 = continue at h+2.
-__device__ __forceinline__ int check_pair(const ulonglong4& sl, uint64_t bits, uint32_t& off, uint32_t& cnt) {
-  if (sl.x == bits) { off = (uint32_t)sl.y; cnt = (uint32_t)(sl.y >> 32); return 1; }
+// `home`: this is the key's home pair, whose overflow flag tells whether a key
+// homed here can live further on.
+__device__ __forceinline__ int check_pair(const ulonglong4& sl, uint64_t bits, uint32_t& off, uint32_t& cnt,
+                                          bool home) {
+  if (sl.x == bits) { off = (uint32_t)sl.y; cnt = (uint32_t)(sl.y >> 32) & kCntMask; return 1; }
   if (sl.x == kEmptyKey) return 0;
-  if (sl.z == bits) { off = (uint32_t)sl.w; cnt = (uint32_t)(sl.w >> 32); return 1; }
+  if (sl.z == bits) { off = (uint32_t)sl.w; cnt = (uint32_t)(sl.w >> 32) & kCntMask; return 1; }
   if (sl.z == kEmptyKey) return 0;
+  if (home && !((sl.y >> 32) & kOverflowBit)) return 0;
   return -1;
 }
 
@@ -746,18 +765,19 @@ struct MatchScratch {
   uint32_t* prow;
   uint32_t* off;
   uint32_t* cnt;
-  uint32_t* wentries;  // per global warp: entries written
-  uint32_t* wpairs;    // per global warp: pairs produced (sum of cnt)
+  uint32_t* wentries;            // per global warp: entries written
+  unsigned long long* wpairs;    // per global warp: pairs produced (sum of cnt; 64-bit, big key groups)
 };
 
 constexpr unsigned kProbeWarps = kProbeThreads / 32;
 
 // Appends one warp tile's hits (probe row, slot.off, slot.cnt) to the warp's
 // scratch run in probe order; returns the tile's pair count.
-__device__ __forceinline__ uint32_t warp_append_hits(unsigned lane, uint64_t first, const uint32_t* off,
+__device__ __forceinline__ uint64_t warp_append_hits(unsigned lane, uint64_t first, const uint32_t* off,
                                                      const uint32_t* cnt, const uint32_t* __restrict__ prows,
                                                      const MatchScratch& sc, uint64_t& cursor) {
-  uint32_t nm = 0, npr = 0;
+  uint32_t nm = 0;
+  uint64_t npr = 0;
 #pragma unroll
   for (int j = 0; j < kWarpItems; ++j) {
     nm += cnt[j] != 0;
@@ -769,7 +789,7 @@ __device__ __forceinline__ uint32_t warp_append_hits(unsigned lane, uint64_t fir
     const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
     if ((int)lane >= o) incl += v;
   }
-  uint32_t tpairs = npr;
+  uint64_t tpairs = npr;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tpairs += __shfl_xor_sync(0xFFFFFFFFu, tpairs, o);
   const uint32_t tmatch = __shfl_sync(0xFFFFFFFFu, incl, 31);
@@ -798,7 +818,7 @@ __device__ __forceinline__ void finish_match_block(unsigned lane, unsigned warp,
                                                    unsigned long long* s_w, unsigned long long* __restrict__ bpart) {
   if (lane == 0) {
     sc.wentries[gw] = (uint32_t)(cursor - lo * kWarpTile);
-    sc.wpairs[gw] = (uint32_t)pairs_total;
+    sc.wpairs[gw] = pairs_total;
     s_w[warp] = pairs_total;
   }
   __syncthreads();
@@ -845,6 +865,7 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_ker
       cnt[j] = 0;
       if (first + j < np) pending |= 1u << j;
     }
+    bool home = true;
     while (pending) {
       ulonglong4 sl[kWarpItems];
 #pragma unroll
@@ -853,10 +874,11 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_ker
 #pragma unroll
       for (int j = 0; j < kWarpItems; ++j) {
         if (!(pending & (1u << j))) continue;
-        const int st = check_pair(sl[j], bits[j], off[j], cnt[j]);
+        const int st = check_pair(sl[j], bits[j], off[j], cnt[j], home);
         if (st >= 0) pending &= ~(1u << j);
         else h[j] = (h[j] + 2) & (uint32_t)mask;
       }
+      home = false;
     }
     pairs_total += warp_append_hits(lane, first, off, cnt, prows, sc, cursor);
   }
@@ -920,6 +942,7 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_prob
         cnt[j] = 0;
         if (base + (uint64_t)j * kProbeThreads < n) pending |= 1u << j;
       }
+      bool home = true;
       while (pending) {
         ulonglong4 sl[kPartProbeItems];
 #pragma unroll
@@ -928,10 +951,11 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_prob
 #pragma unroll
         for (int j = 0; j < kPartProbeItems; ++j) {
           if (!(pending & (1u << j))) continue;
-          const int st = check_pair(sl[j], bits[j], off[j], cnt[j]);
+          const int st = check_pair(sl[j], bits[j], off[j], cnt[j], home);
           if (st >= 0) pending &= ~(1u << j);
           else h[j] = (h[j] + 2) & (uint32_t)mask;
         }
+        home = false;
       }
 #pragma unroll
       for (int j = 0; j < kPartProbeItems; ++j) {
@@ -1077,10 +1101,10 @@ __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch s
     }
 #pragma unroll
     for (int q = 0; q < kBatch; ++q) {
-      uint32_t incl = c[q];
+      uint64_t incl = c[q];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        const uint64_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if ((int)lane >= o) incl += v;
       }
       unsigned long long g = run + (incl - c[q]);

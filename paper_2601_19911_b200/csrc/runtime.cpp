@@ -4,18 +4,13 @@
 
 namespace golp {
 
-static std::mutex g_err_mu;
-static std::string g_err;
+// Per thread: threads driving different contexts (B200Device(gpus=G)) report
+// their own failures.
+static thread_local std::string t_err;
 
-void set_error(const std::string& msg) {
-  std::lock_guard<std::mutex> lk(g_err_mu);
-  g_err = msg;
-}
+void set_error(const std::string& msg) { t_err = msg; }
 
-const char* last_error_cstr() {
-  std::lock_guard<std::mutex> lk(g_err_mu);
-  return g_err.c_str();
-}
+const char* last_error_cstr() { return t_err.c_str(); }
 
 double wall_seconds() {
   using clk = std::chrono::steady_clock;

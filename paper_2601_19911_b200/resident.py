@@ -14,6 +14,13 @@ import torch
 from . import _native
 
 
+def _lib(t: torch.Tensor):
+    """The library with the context of t's device current on this thread."""
+    lib = _native.load()
+    _native.check(lib.golp_use_device(t.device.index if t.device.index is not None else 0))
+    return lib
+
+
 def _stream(stream) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return int(s.cuda_stream)
@@ -41,7 +48,7 @@ def topk(keys: torch.Tensor, rows: torch.Tensor, k: int, stream=None, want_codes
     kk = min(k, n)
     out = torch.empty(kk, dtype=torch.int32, device=keys.device)
     codes = torch.empty(kk, dtype=torch.int64, device=keys.device) if want_codes else None
-    lib = _native.load()
+    lib = _lib(keys)
     _native.check(lib.golp_topk_device(keys.data_ptr(), rows.data_ptr(), n, k, out.data_ptr() if kk else 0,
                                        codes.data_ptr() if (codes is not None and kk) else 0, _stream(stream)))
     return out, codes
@@ -55,7 +62,7 @@ def merge(codes: torch.Tensor, rows: torch.Tensor, k: int, stream=None, want_cod
     kk = min(k, n)
     out = torch.empty(kk, dtype=torch.int32, device=codes.device)
     oc = torch.empty(kk, dtype=torch.int64, device=codes.device) if want_codes else None
-    lib = _native.load()
+    lib = _lib(codes)
     _native.check(lib.golp_topk_merge_device(codes.data_ptr(), rows.data_ptr(), n, k, out.data_ptr() if kk else 0,
                                              oc.data_ptr() if (oc is not None and kk) else 0, _stream(stream)))
     return out, oc
@@ -63,7 +70,7 @@ def merge(codes: torch.Tensor, rows: torch.Tensor, k: int, stream=None, want_cod
 
 def join_build(keys: torch.Tensor, rows: torch.Tensor, stream=None) -> None:
     _check_cols(keys, rows)
-    _native.check(_native.load().golp_join_build_device(keys.data_ptr(), rows.data_ptr(), keys.numel(),
+    _native.check(_lib(keys).golp_join_build_device(keys.data_ptr(), rows.data_ptr(), keys.numel(),
                                                         _stream(stream)))
 
 
@@ -74,7 +81,7 @@ def join_probe(keys: torch.Tensor, rows: torch.Tensor, out_probe: torch.Tensor, 
     _check_cols(keys, rows)
     cap = min(out_probe.numel(), out_build.numel())
     m = C.c_uint64(0)
-    _native.check(_native.load().golp_join_probe_device(keys.data_ptr(), rows.data_ptr(), keys.numel(),
+    _native.check(_lib(keys).golp_join_probe_device(keys.data_ptr(), rows.data_ptr(), keys.numel(),
                                                         out_probe.data_ptr(), out_build.data_ptr(), cap,
                                                         C.byref(m), _stream(stream)))
     return int(m.value)
@@ -87,7 +94,7 @@ def join_probe_async(keys: torch.Tensor, rows: torch.Tensor, out_probe: torch.Te
     buffers' capacity are dropped: compare matches with the capacity afterwards."""
     _check_cols(keys, rows)
     cap = min(out_probe.numel(), out_build.numel())
-    _native.check(_native.load().golp_join_probe_device_async(keys.data_ptr(), rows.data_ptr(), keys.numel(),
+    _native.check(_lib(keys).golp_join_probe_device_async(keys.data_ptr(), rows.data_ptr(), keys.numel(),
                                                               out_probe.data_ptr(), out_build.data_ptr(), cap,
                                                               matches.data_ptr(), _stream(stream)))
 
@@ -100,7 +107,7 @@ def join(bkeys, brows, pkeys, prows, capacity: int | None = None, stream=None):
         op = torch.empty(cap, dtype=torch.int32, device=pkeys.device)
         ob = torch.empty(cap, dtype=torch.int32, device=pkeys.device)
         m = C.c_uint64(0)
-        lib = _native.load()
+        lib = _lib(pkeys)
         rc = lib.golp_join_probe_device(pkeys.data_ptr(), prows.data_ptr(), pkeys.numel(), op.data_ptr(),
                                         ob.data_ptr(), cap, C.byref(m), _stream(stream))
         if rc == _native.GOLP_ERR_CAPACITY:
@@ -115,7 +122,7 @@ def full_sort(keys: torch.Tensor, rows: torch.Tensor, stream=None) -> torch.Tens
     row id -- host_full_sort (pkg/src/golp/host.py:127-130) on the device."""
     _check_cols(keys, rows)
     out = torch.empty(keys.numel(), dtype=torch.int32, device=keys.device)
-    _native.check(_native.load().golp_full_sort_device(keys.data_ptr(), rows.data_ptr(), keys.numel(),
+    _native.check(_lib(keys).golp_full_sort_device(keys.data_ptr(), rows.data_ptr(), keys.numel(),
                                                        out.data_ptr() if keys.numel() else 0, _stream(stream)))
     return out
 
