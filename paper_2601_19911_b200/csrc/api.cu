@@ -17,7 +17,6 @@
 
 #include "../../include/golp_b200.h"
 #include "join.cuh"
-#include "probe.cuh"
 #include "runtime.h"
 #include "sort.cuh"
 #include "topk.cuh"
@@ -117,8 +116,6 @@ struct Ctx {
   DevBuf sc_prow, sc_off, sc_cnt;
   DevBuf part_keys, part_pos, part_cnt, part_cur, run_base, run_len, res_part, work_ctr;
   DevBuf pairs_p, pairs_b;
-  DevBuf fstat;             // direct probe: ticket, staging bump, per-tile counts / staged offsets
-  DevBuf stage_p, stage_b;  // direct probe: pair staging area
   DevBuf rows_flag;  // build row column is a dense run (join_build_impl)
   DevBuf row_base;   // what the emit adds to a singleton's slot.off (rows[0] for a dense column, else 0)
   DevBuf srt_hist, srt_k0, srt_k1, srt_r0, srt_r1, srt_status, srt_base;
@@ -1072,62 +1069,11 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   return GOLP_OK;
 }
 
-// Direct probe of [pkeys, pkeys+np) (probe.cuh): warp tiles look up and stage
-// their pairs (one launch), tile counts are scanned into output offsets chained
-// after *base_in, the staged runs are placed. *total_out = *base_in + pairs.
-// Pairs at positions >= cap are counted, not written.
-int launch_probe_direct(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
-                        uint64_t cap, const unsigned long long* base_in, unsigned long long* total_out,
-                        cudaStream_t s) {
-  Ctx& g = cur();
-  const uint64_t ntiles = (np + kPSpan - 1) / kPSpan;
-  const uint64_t nplace = (ntiles + kPlaceTiles - 1) / kPlaceTiles;
-  CK(g.fstat.ensure((2 + nplace + 2 * ntiles) * 8));
-  // [0] ticket, [1] staging bump, [2, 2+nplace) placement look-back words, then per tile
-  unsigned long long* ctr = g.fstat.as<unsigned long long>();
-  unsigned long long* place_status = ctr + 2;
-  unsigned long long* tile_count = place_status + nplace;
-  unsigned long long* tile_stage = tile_count + ntiles;
-  CK(cudaMemsetAsync(ctr, 0, (2 + nplace) * 8, s));
-  const uint64_t stage_cap = std::max<uint64_t>(cap, 1);
-  CK(g.stage_p.ensure(stage_cap * 4));
-  CK(g.stage_b.ensure(stage_cap * 4));
-  const int per = blocks_per_sm(join_probe_lookup_kernel, kPThreads, kPSmem);
-  if (per < 1) {
-    set_error("join_probe_lookup_kernel cannot be resident");
-    return GOLP_ERR_CUDA;
-  }
-  const uint64_t grid = std::min<uint64_t>((ntiles + kPWarps - 1) / kPWarps, (uint64_t)per * g.sms);
-  ProbeLookupArgs a;
-  a.keys = pkeys;
-  a.rows = prows;
-  a.np = np;
-  a.table = g.table.as<Slot>();
-  a.mask = (uint32_t)g.jmask;
-  a.csr_row = g.rows_arr.as<uint32_t>();
-  a.row_base = g.row_base.as<uint32_t>();
-  a.stage_p = g.stage_p.as<uint32_t>();
-  a.stage_b = g.stage_b.as<uint32_t>();
-  a.stage_cap = stage_cap;
-  a.ticket = ctr;
-  a.bump = ctr + 1;
-  a.tile_count = tile_count;
-  a.tile_stage = tile_stage;
-  join_probe_lookup_kernel<<<(unsigned)grid, kPThreads, kPSmem, s>>>(a);
-  CKL();
-  join_probe_place_kernel<<<(unsigned)nplace, kPlaceThreads, 0, s>>>(a.stage_p, a.stage_b, stage_cap, tile_count,
-                                                                  tile_stage, ntiles, place_status, base_in,
-                                                                  total_out, out_p, out_b, cap);
-  CKL();
-  g_launches += 2;
-  return GOLP_OK;
-}
-
-// One probe over [pkeys, pkeys+np). Tables probed directly: launch_probe_direct.
-// Radix-partitioned probes (C4-sized tables): per span, partition + slice-
-// ordered lookups, then match -> scan of block totals -> emit per sub-chunk
-// (the sub-chunk bounds the scratch). Pair offsets continue from *base_in;
-// *total_out = *base_in + pairs of this call.
+// One probe over [pkeys, pkeys+np): match -> scan of block totals -> emit, per
+// sub-chunk (the sub-chunk bounds the scratch); radix-partitioned probes
+// (C4-sized tables) first partition each span and look its keys up slice by
+// slice. Pair offsets continue from *base_in; *total_out = *base_in + pairs of
+// this call.
 int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
                  uint64_t cap, const unsigned long long* base_in, unsigned long long* total_out, cudaStream_t s) {
   Ctx& g = cur();
@@ -1142,8 +1088,6 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
   const uint64_t force = env_u64("GOLP_JOIN_PART_PROBE", 2);
   const bool part_probe =
       g.jparts > 1 && (force == 1 || (force == 2 && std::min(np, kSpan) >= g.jcap));
-  if (!part_probe && env_u64("GOLP_JOIN_DIRECT", 1))
-    return launch_probe_direct(pkeys, prows, np, out_p, out_b, cap, base_in, total_out, s);
   constexpr uint64_t kSub = 1ull << 27;  // probes per sub-chunk (scratch <= 1.5 GiB)
   const uint64_t sub = std::min(np, kSub);
   const uint64_t nwt_max = (sub + kWarpTile - 1) / kWarpTile;
@@ -1350,7 +1294,7 @@ void release_context(Ctx& g) {
   g.pool.stop();
   DevBuf* bufs[] = {&g.ctl, &g.cand_hi, &g.cand_lo, &g.w_hi, &g.w_lo, &g.out_rows, &g.out_hi, &g.samples,
                     &g.table, &g.rows_arr, &g.ovf, &g.big_list, &g.jcount,
-                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.fstat, &g.stage_p, &g.stage_b, &g.srt_hist, &g.srt_k0, &g.srt_k1, &g.srt_r0, &g.srt_r1, &g.srt_status, &g.srt_base, &g.in_keys, &g.in_rows,
+                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.srt_hist, &g.srt_k0, &g.srt_k1, &g.srt_r0, &g.srt_r1, &g.srt_status, &g.srt_base, &g.in_keys, &g.in_rows,
                     &g.in_bkeys, &g.in_brows, &g.in_payload, &g.rows_flag, &g.row_base};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < kSlots; ++i) {

@@ -16,7 +16,7 @@ PKG = HERE.parent
 ROOT = PKG.parent
 LIB = PKG / "libgolp_b200.so"
 SOURCES = ["api.cu", "host_engine.cpp", "runtime.cpp"]
-HEADERS = ["common.cuh", "sortnet.cuh", "topk.cuh", "sort.cuh", "join.cuh", "probe.cuh", "runtime.h"]
+HEADERS = ["common.cuh", "sortnet.cuh", "topk.cuh", "sort.cuh", "join.cuh", "runtime.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [
