@@ -158,7 +158,19 @@ int golp_host_gather(const void* src, uint64_t row_bytes, uint64_t nrows, const 
       }
       return;
     }
+    // Rows are random in a table far larger than the caches: prefetch the rows
+    // kAhead ids ahead (every cache line of each) so that many misses overlap.
+    constexpr uint64_t kAhead = 16;
+    auto prefetch_row = [&](uint64_t i) {
+      const uint32_t r = ids[i];
+      if (r >= nrows) return;
+      const char* p = s + (uint64_t)r * row_bytes;
+      for (uint64_t o = 0; o < row_bytes; o += 64) __builtin_prefetch(p + o, 0, 0);
+      __builtin_prefetch(p + row_bytes - 1, 0, 0);
+    };
+    for (uint64_t i = lo; i < std::min(hi, lo + kAhead); ++i) prefetch_row(i);
     for (uint64_t i = lo; i < hi; ++i) {
+      if (i + kAhead < hi) prefetch_row(i + kAhead);
       const uint32_t r = ids[i];
       if (r >= nrows) { bad = true; return; }
       std::memcpy(d + i * row_bytes, s + (uint64_t)r * row_bytes, row_bytes);

@@ -260,3 +260,20 @@ def test_k_aware_gate_fixes_the_reference_forms_misses():
     assert decide(GateConfig(cpu_model=ext, profile=prof), OP_TOPK, n, k).path == DEVICE
     assert decide(GateConfig(cpu_model=ref, profile=prof), OP_PROBE, 1000, 500, None, 100).path == DEVICE
     assert decide(GateConfig(cpu_model=ext, profile=prof), OP_PROBE, 1000, 500, None, 100).path == HOST
+
+
+def test_materialize_joins_on_the_query_path_cpu():
+    """GateConfig(materialize_joins=True): the probe query returns both sides
+    gathered in pair order, on the modeled (virtual-clock) device and the host path."""
+    from paper_2601_19911_b200 import DEVICE, HOST, OP_PROBE, GateConfig, ModeledDevice, execute_path, generate_table
+    from paper_2601_19911_b200.store import ColumnTable, MaterializedJoin
+
+    bt, pt = generate_table(300, 4, seed=3), generate_table(2_000, 4, seed=4)
+    # the probe table starts with the build keys, so that pairs exist
+    pt = ColumnTable(np.concatenate([bt.key_column, pt.key_column])[:2_000], pt.payload_column, 4)
+    for path in (DEVICE, HOST):
+        res, lat = execute_path((bt, pt), OP_PROBE, 1, GateConfig(materialize_joins=True), ModeledDevice(), path)
+        assert isinstance(res, MaterializedJoin) and len(res) >= 300 and lat > 0
+        assert np.array_equal(res.probe.keys, res.build.keys)
+        assert np.array_equal(res.probe.payloads, pt.payload_column[res.probe.row_ids])
+        assert np.array_equal(res.build.payloads, bt.payload_column[res.build.row_ids])

@@ -55,3 +55,37 @@ def test_scaling_baseline_with_b200_rows(b200):
     ops = {(r.n, r.op) for r in rows}
     assert (200_000, "full_sort@b200") in ops and (200_000, "topk@b200") in ops
     assert all(r.median_s > 0 for r in rows)
+
+
+def _join_tables(nb, np_, payload_bytes, seed):
+    """Build / probe ColumnTables with C2-style join keys (uniform integers in [0, 2*nb) as f8)."""
+    from paper_2601_19911_b200.store import ColumnTable
+
+    rng = np.random.Generator(np.random.PCG64(seed))
+    bk = rng.integers(0, 2 * nb, size=nb).astype(np.float64)
+    pk = rng.integers(0, 2 * nb, size=np_).astype(np.float64)
+    bp = (np.arange(nb * payload_bytes, dtype=np.uint64) * 2654435761 % 251).astype(np.uint8).reshape(nb, payload_bytes)
+    pp = (np.arange(np_ * payload_bytes, dtype=np.uint64) * 40503 % 241).astype(np.uint8).reshape(np_, payload_bytes)
+    return ColumnTable(bk, bp, seed), ColumnTable(pk, pp, seed + 1)
+
+
+@pytest.mark.parametrize("path", [DEVICE, HOST])
+def test_join_late_materialization_on_the_query_path_c2(b200, path):
+    """execute_path with materialize_joins: pairs in reference order, then both
+    sides' keys + payloads gathered in pair order (store.materialize semantics,
+    pkg/src/golp/store.py:184-201), at the C2 shape (build 1e6 / probe 1e7)."""
+    from oracle import oracle
+
+    nb, np_ = (1_000_000, 10_000_000) if path == DEVICE else (100_000, 1_000_000)
+    bt, pt = _join_tables(nb, np_, 16, seed=1)
+    cfg = GateConfig(materialize_joins=True)
+    res, lat = execute_path((bt, pt), OP_PROBE, 1, cfg, b200, path)
+    ep, eb = oracle.join(bt.key_column, bt.positions, pt.key_column, pt.positions)
+    assert len(res) == len(ep) and lat > 0
+    assert np.array_equal(res.probe.row_ids, ep) and np.array_equal(res.build.row_ids, eb)
+    assert np.array_equal(res.probe.keys, pt.key_column[ep]) and np.array_equal(res.build.keys, bt.key_column[eb])
+    assert np.array_equal(res.probe.keys, res.build.keys)  # an equi-join
+    assert np.array_equal(res.probe.payloads, pt.payload_column[ep])
+    assert np.array_equal(res.build.payloads, bt.payload_column[eb])
+    assert GateConfig.from_json_dict(cfg.to_json_dict()) == cfg
+    assert "materialize_joins" not in GateConfig().to_json_dict()
