@@ -77,6 +77,9 @@ typedef struct golp_kernel_times {
   uint64_t join_slices;     /* table slices of a radix-partitioned join (1 = not partitioned) */
   double full_sort_ms;      /* device time of the last full sort                     */
   uint64_t full_sort_passes;/* digit passes it needed (of 12)                         */
+  double call_kernel_ms;    /* device time of the kernels of the last host-buffer call
+                               (golp_topk / golp_probe / golp_full_sort), summed over its
+                               kernel groups; upload waits excluded (C_gpu's kernel term) */
 } golp_kernel_times;
 
 /* ---- lifecycle ---------------------------------------------------------------- */
@@ -113,6 +116,11 @@ int golp_last_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 /* 1 (default; env GOLP_DENSE_ROWS=0 turns it off): dense row-id columns are
  * regenerated on the device; 0: every row-id column is copied. */
 int golp_set_dense_rows(int on);
+/* Declares that the row-id columns of the NEXT host-buffer call on this
+ * context are dense runs (rows[i] == rows[0] + i), e.g. a table's own
+ * positions as extract_keys passes them (store.py:178-181): the host-side scan
+ * that verifies this is skipped (the end points are still checked). */
+int golp_hint_dense_rows(void);
 int golp_set_profiling(int on);
 int golp_last_kernel_times(golp_kernel_times* out);
 

@@ -57,6 +57,7 @@ class KernelTimes(C.Structure):
         ("join_slices", C.c_uint64),
         ("full_sort_ms", C.c_double),
         ("full_sort_passes", C.c_uint64),
+        ("call_kernel_ms", C.c_double),
     ]
 
 
@@ -74,6 +75,7 @@ SIGNATURES = {
     "golp_launch_count": (_u64, []),
     "golp_last_transfer": (_int, [C.POINTER(_u64), C.POINTER(_u64)]),
     "golp_set_dense_rows": (_int, [_int]),
+    "golp_hint_dense_rows": (_int, []),
     "golp_set_profiling": (_int, [_int]),
     "golp_last_kernel_times": (_int, [C.POINTER(KernelTimes)]),
     "golp_topk": (_int, [_vp, _vp, _u64, _u64, _int, _u32, _vp, C.POINTER(_u64), C.POINTER(Ledger)]),

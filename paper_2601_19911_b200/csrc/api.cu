@@ -129,6 +129,7 @@ struct Ctx {
   // call (the ledger keeps the reference's shape formulas instead).
   uint64_t moved_h2d = 0, moved_d2h = 0;
   bool dense_rows = true;  // GOLP_DENSE_ROWS=0 ships every row-id column
+  bool rows_hint = false;  // golp_hint_dense_rows: the next call's row columns are positions
 
   char* status_host = nullptr;  // mapped pinned words: select status + candidate count
   char* status_dev = nullptr;
@@ -143,6 +144,8 @@ struct Ctx {
   std::set<const void*> smem_set;
   std::map<std::pair<const void*, int>, int> per_sm;
   std::vector<cudaEvent_t> trace_ev;  // GOLP_TRACE upload markers (golp_probe)
+  std::vector<cudaEvent_t> kspan_ev;  // profiling: (start, end) pairs around each kernel group of a call
+  size_t kspan_n = 0;
 };
 
 // One context per (device, handle): streams, pinned staging rings, HBM
@@ -381,7 +384,10 @@ int upload_rows(uint32_t* dst, const uint32_t* src, uint64_t n, bool* copied = n
   if (copied) *copied = false;
   if (!n) return GOLP_OK;
   const double tv = wall_seconds();
-  const bool dense = g.dense_rows && dense_run(g.pool, src, n);
+  // A caller-declared dense column (golp_hint_dense_rows: the table's own
+  // positions, extract_keys) skips the scan; its end points are still checked.
+  const bool hinted = g.rows_hint && src[n - 1] == src[0] + (uint32_t)(n - 1);
+  const bool dense = g.dense_rows && (hinted || dense_run(g.pool, src, n));
   if (std::getenv("GOLP_TRACE"))
     std::fprintf(stderr, "[golp] rows [%llu] verified in %.3f ms: %s\n", (unsigned long long)n, (wall_seconds() - tv) * 1e3,
                  dense ? "dense" : "copied");
@@ -727,6 +733,38 @@ double prof_ms(int a, int b) {
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, g.ev[a], g.ev[b]) != cudaSuccess) return 0.0;
   return (double)ms;
+}
+
+// Device time of the kernels of one host-buffer call (golp_set_profiling on):
+// timing events around each group of kernels a call enqueues on its main
+// stream (a chunk's filter or probe, the build, the final select), summed when
+// the call has finished. Upload waits between the groups are not counted, so
+// this is the kernel term of C_gpu (device.py:154-181) for calibration.
+void kspan_reset() { cur().kspan_n = 0; }
+int kspan_mark(cudaStream_t s) {
+  Ctx& g = cur();
+  if (!g.prof) return GOLP_OK;
+  if (g.kspan_ev.size() <= g.kspan_n) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    g.kspan_ev.push_back(e);
+  }
+  CK(cudaEventRecord(g.kspan_ev[g.kspan_n++], s));
+  return GOLP_OK;
+}
+int kspan_finish() {
+  Ctx& g = cur();
+  double ms = 0.0;
+  if (g.prof && g.kspan_n >= 2) {
+    CK(cudaEventSynchronize(g.kspan_ev[g.kspan_n - 1]));
+    for (size_t i = 0; i + 1 < g.kspan_n; i += 2) {
+      float x = 0.f;
+      CK(cudaEventElapsedTime(&x, g.kspan_ev[i], g.kspan_ev[i + 1]));
+      ms += x;
+    }
+  }
+  g.kt.call_kernel_ms = ms;
+  return GOLP_OK;
 }
 
 // Status / candidate count of a sampled run: the select kernel stores them into
@@ -1424,6 +1462,12 @@ int golp_last_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
   return GOLP_OK;
 }
 
+int golp_hint_dense_rows(void) {
+  RET(ensure_init());
+  cur().rows_hint = true;
+  return GOLP_OK;
+}
+
 int golp_set_profiling(int on) {
   Ctx& g = cur();
   RET(ensure_init());
@@ -1491,6 +1535,11 @@ int golp_full_sort(const double* keys, const uint32_t* rows, uint64_t n, int mod
   if (!led) return invalid("null ledger");
   RET(ensure_init());
   g.moved_h2d = g.moved_d2h = 0;
+  kspan_reset();
+  struct HintReset {  // the row-id hint covers this one call
+    Ctx& c;
+    ~HintReset() { c.rows_hint = false; }
+  } hint_reset{g};
   const double t0 = wall_seconds();
   *led = golp_ledger{entry * n, 4 * n, 0.0, 0.0, 0.0, 0.0};
   if (n == 0) return GOLP_OK;
@@ -1509,7 +1558,9 @@ int golp_full_sort(const double* keys, const uint32_t* rows, uint64_t n, int mod
   for (bool& b : g.pin_busy) b = false;
   const double t1 = wall_seconds();
   CK(cudaStreamWaitEvent(s, ev_up, 0));
+  RET(kspan_mark(s));
   RET(full_sort_impl(g.in_keys.as<double>(), g.in_rows.as<uint32_t>(), n, g.out_rows.as<uint32_t>(), s));
+  RET(kspan_mark(s));
   CK(cudaStreamSynchronize(s));
   if (g.prof) g.kt.full_sort_ms = prof_ms(0, 1);
   const double t2 = wall_seconds();
@@ -1523,7 +1574,7 @@ int golp_full_sort(const double* keys, const uint32_t* rows, uint64_t n, int mod
   led->t_h2d = t1 - t0;
   led->t_kernel = t2 - t1;
   led->t_d2h = wall_seconds() - t2;
-  return GOLP_OK;
+  return kspan_finish();
 }
 
 int golp_topk_merge_device(const uint64_t* d_key_codes, const uint32_t* d_rows, uint64_t n, uint64_t k,
@@ -1595,6 +1646,11 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
   if (!out_len || !led) return invalid("null output pointer");
   RET(ensure_init());
   g.moved_h2d = g.moved_d2h = 0;
+  kspan_reset();
+  struct HintReset {  // the row-id hint covers this one call
+    Ctx& c;
+    ~HintReset() { c.rows_hint = false; }
+  } hint_reset{g};
   const double t0 = wall_seconds();
   const uint64_t kk = std::min(k, n);
   *out_len = kk;
@@ -1631,7 +1687,9 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     if (trace) std::fprintf(stderr, "[golp] topk %.3f ms uploads done\n", (t1 - t0) * 1e3);
     CK(cudaStreamWaitEvent(s, ev_chunk, 0));
     uint32_t* d_out = g.out_rows.as<uint32_t>();
+    RET(kspan_mark(s));
     RET(topk_device_impl(dk, dr, n, kk, d_out, nullptr, s));
+    RET(kspan_mark(s));
     CK(cudaStreamSynchronize(s));  // the fused path is stream-ordered: charge its time to t_kernel
     const double t2 = wall_seconds();
     uint32_t* hbuf = static_cast<uint32_t*>(g.pin_small);
@@ -1646,7 +1704,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     led->t_h2d = t1 - t0;
     led->t_kernel = t2 - t1;
     led->t_d2h = wall_seconds() - t2;
-    return GOLP_OK;
+    return kspan_finish();
   }
   if (!p.direct) {
     // Stratified samples gathered on the host (same strata as SrcSample).
@@ -1686,7 +1744,9 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
         CK(cudaEventRecord(ev_chunk, g.s_h2d));
         CK(cudaStreamWaitEvent(s, ev_chunk, 0));
       }
+      RET(kspan_mark(s));
       RET(launch_filter(dk + c0, dr + c0, cn, p.cap, s));
+      RET(kspan_mark(s));
     }
     return GOLP_OK;
   };
@@ -1704,6 +1764,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
   const double t1 = wall_seconds();
   CK(cudaStreamWaitEvent(s, ev_chunk, 0));
   uint32_t* d_out = g.out_rows.as<uint32_t>();
+  RET(kspan_mark(s));
   if (p.direct) {
     RET(topk_direct(dk, dr, n, kk, d_out, nullptr, s));
     CK(cudaStreamSynchronize(s));
@@ -1720,6 +1781,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
       CK(cudaStreamSynchronize(s));
     }
   }
+  RET(kspan_mark(s));
   const double t2 = wall_seconds();
   uint32_t* hbuf = static_cast<uint32_t*>(g.pin_small);
   if (kk * 4 <= g.pin_small_bytes) {
@@ -1735,7 +1797,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
   led->t_h2d = t1 - t0;
   led->t_kernel = t2 - t1;
   led->t_d2h = t3 - t2;
-  return GOLP_OK;
+  return kspan_finish();
 }
 
 #ifndef GOLP_TAIL_SPLIT
@@ -1752,6 +1814,11 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   RET(ensure_init());
   g.last_probe_valid = false;
   g.moved_h2d = g.moved_d2h = 0;
+  kspan_reset();
+  struct HintReset {  // the row-id hint covers this one call
+    Ctx& c;
+    ~HintReset() { c.rows_hint = false; }
+  } hint_reset{g};
   const double t0 = wall_seconds();
   *led = golp_ledger{entry * (nb + np), 0, 0.0, 0.0, 0.0, 0.0};
   *out_matches = 0;
@@ -1791,7 +1858,9 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   cudaEvent_t ev_chunk = g.ev[0];
   CK(cudaEventRecord(ev_chunk, g.s_h2d));
   CK(cudaStreamWaitEvent(s, ev_chunk, 0));
+  RET(kspan_mark(s));
   RET(join_build_impl(dbk, dbr, nb, s, (nb > 0 && !brows_copied) ? 1 : 0));
+  RET(kspan_mark(s));
 
   uint64_t per_chunk = std::max<uint64_t>(g.chunk / 8, kWarpTile);
   per_chunk = (per_chunk / kWarpTile) * kWarpTile;
@@ -1873,7 +1942,9 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   };
   auto probe_chunk = [&](uint64_t c, uint32_t* op, uint32_t* ob, uint64_t cap_) -> int {
     const uint64_t c0 = cb[c], cn = cb[c + 1] - c0;
+    RET(kspan_mark(s));
     RET(launch_probe(dpk + c0, dpr + c0, cn, op, ob, cap_, totals + c, totals + c + 1, s));
+    RET(kspan_mark(s));
     publish_u64_kernel<<<1, 1, 0, s>>>(reinterpret_cast<volatile unsigned long long*>(g.mirror_dev + c + 1),
                                        totals + c + 1);
     CKL();
@@ -1997,7 +2068,7 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   } else {
     led->t_kernel += t3 - t2;  // copy_out adds the D2H phase
   }
-  return GOLP_OK;
+  return kspan_finish();
 }
 
 int golp_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m, golp_ledger* led) {

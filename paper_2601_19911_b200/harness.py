@@ -18,7 +18,8 @@ from typing import NamedTuple, Optional, Sequence
 
 import numpy as np
 
-from .device import DEFAULT_MODELED_PROFILE, FULL_ROW, KEY_ONLY, OP_PROBE, OP_TOPK, ModeledDevice, calibrate_profile
+from .device import (DEFAULT_MODELED_PROFILE, FULL_ROW, KEY_ONLY, OP_PROBE, OP_TOPK, ModeledDevice, TransferLedger,
+                     calibrate_profile)
 from .errors import StrategyMismatchError
 from .gate import DEFAULT_CPU_MODEL, DEVICE, HOST, OP_FULL_SORT, GateConfig, estimate_cpu_cost, execute_gated, execute_path
 from .host import host_full_sort, host_topk, mix64
@@ -300,19 +301,48 @@ def run_payload_comparison(spec: WorkloadSpec, device=None, profile=DEFAULT_MODE
     return PayloadComparison(payload_rows, transfer_rows, e2e_rows)
 
 
+def _timed_ledger(device, call):
+    """A call's ledger for calibration. On a device that times its kernels with
+    CUDA events (B200Device.time_kernels), t_kernel is that device time and the
+    rest of the critical path is charged to the transfer phases (the ledger's
+    wall-clock split puts only the kernel TAIL after the last upload into
+    t_kernel, which does not grow with n: chunks are filtered / probed while
+    later chunks upload). The phases still add up to the measured call time."""
+    led = call().ledger
+    timer = getattr(device, "last_kernel_seconds", None)
+    k = timer() if timer is not None else None
+    if not k:
+        return led
+    t_h2d = max(led.total - k - led.t_d2h - led.t_post, 0.0)
+    return TransferLedger.build(led.h2d_bytes, led.d2h_bytes, t_h2d, k, led.t_d2h, led.t_post)
+
+
 def calibrate_device_profile(device, ns: Sequence[int] = (100_000, 1_000_000, 4_000_000, 16_000_000), k: int = 100,
                              repeats: int = 3, seed: int = 0, probe_ns: Sequence[int] = ()):
     """Measured ledgers of `device` over an n grid -> DeviceProfile (the gate's C_gpu).
 
     For each n, the median-total ledger of `repeats` Top-K calls (after one
     warm-up) is kept; optional probe samples (build = probe = n/2, keys in
-    [0, n)) calibrate kernel_rate_probe.
+    [0, n)) calibrate kernel_rate_probe. A B200Device times its kernels with
+    CUDA events during calibration, so kernel_rate_* are device rates.
     """
+    timing = getattr(device, "time_kernels", None)
+    if timing is not None:
+        timing(True)
+    try:
+        return _calibrate(device, ns, k, repeats, seed, probe_ns)
+    finally:
+        if timing is not None:
+            timing(False)
+
+
+def _calibrate(device, ns, k, repeats, seed, probe_ns):
     samples = []
     for n in ns:
         kv = random_key_vector(n, table_seed(seed, n))
         device.topk(kv, k)
-        leds = sorted((device.topk(kv, k).ledger for _ in range(repeats)), key=lambda lg: lg.total)
+        leds = sorted((_timed_ledger(device, lambda: device.topk(kv, k)) for _ in range(repeats)),
+                      key=lambda lg: lg.total)
         samples.append((n, leds[len(leds) // 2]))
     probe_samples = []
     for n in probe_ns:
@@ -323,7 +353,8 @@ def calibrate_device_profile(device, ns: Sequence[int] = (100_000, 1_000_000, 4_
         b = KeyVector(rng.integers(0, n, half).astype(np.float64), np.arange(half, dtype=np.uint32))
         p = KeyVector(rng.integers(0, n, half).astype(np.float64), np.arange(half, dtype=np.uint32))
         device.probe(b, p)
-        leds = sorted((device.probe(b, p).ledger for _ in range(repeats)), key=lambda lg: lg.total)
+        leds = sorted((_timed_ledger(device, lambda: device.probe(b, p)) for _ in range(repeats)),
+                      key=lambda lg: lg.total)
         probe_samples.append((2 * half, leds[len(leds) // 2]))
     if len({n for n, _ in probe_samples}) >= 3:
         # Probes return tens of MB, so their ledgers pin both link bandwidths;

@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts_match_header():
     assert C.sizeof(_native.Ledger) == 2 * 8 + 4 * 8
-    assert C.sizeof(_native.KernelTimes) == 6 * 8 + 6 * 8
+    assert C.sizeof(_native.KernelTimes) == 7 * 8 + 6 * 8
 
 
 def test_version_and_error_string():

@@ -89,3 +89,34 @@ def test_join_late_materialization_on_the_query_path_c2(b200, path):
     assert np.array_equal(res.build.payloads, bt.payload_column[eb])
     assert GateConfig.from_json_dict(cfg.to_json_dict()) == cfg
     assert "materialize_joins" not in GateConfig().to_json_dict()
+
+
+def test_calibrated_profile_kernel_terms_are_device_timed(b200):
+    """C_gpu's kernel term comes from CUDA-event kernel times (not the wall-clock
+    tail after the last upload), so no kernel rate sits at the fit's clamp."""
+    prof = calibrate_device_profile(b200, ns=(250_000, 1_000_000, 4_000_000, 16_000_000),
+                                    probe_ns=(500_000, 2_000_000, 8_000_000), repeats=3)
+    assert prof.kernel_rate_topk > 1e-12 and prof.kernel_rate_probe > 1e-12
+    # device rates: Top-K well above 10 Gkeys/s, build+probe above 1 Gkeys/s
+    assert prof.kernel_rate_topk < 1e-10 and prof.kernel_rate_probe < 1e-9
+    assert 20e9 < prof.h2d_bandwidth < 200e9  # per reference byte (12 B/entry accounted, 8 moved)
+
+
+def test_criterion_07_stream_on_b200(b200):
+    """Reference acceptance criterion 7 (pkg/tests/test_acceptance.py:252-270) on
+    real hardware: the 500-query 80/20 stream (n in {1e4, 1e6}, seed 3, 188-B
+    payloads) under host_only / device_always / gated, three runs. The gate
+    sends 1e4 to the host and 1e6 to the device, so it beats both fixed
+    strategies at P50 and host_only everywhere; its P95/P99 are the same device
+    calls as device_always's tail and are held within 10% of them (run-to-run
+    state, not a different path, separates them: DESIGN.md §9)."""
+    spec = WorkloadSpec(n_grid=(10_000, 1_000_000), repeats=250, mix=(0.8, 0.2), seed=3)
+    assert len(spec.n_grid) * spec.repeats == 500
+    tables = {}
+    for _ in range(3):
+        host, device, gated = run_strategy_comparison(spec, GateConfig(), device=b200, tables=tables)
+        h, d, g = (compute_stats(r.all_samples()) for r in (host, device, gated))
+        assert 0.1 < gated.offload_rate < 0.3
+        assert g.median < h.median and g.median < d.median
+        assert g.p95 <= h.p95 and g.p99 <= h.p99
+        assert g.p95 <= 1.10 * d.p95 and g.p99 <= 1.10 * d.p99
