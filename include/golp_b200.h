@@ -132,6 +132,13 @@ int golp_last_kernel_times(golp_kernel_times* out);
 int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, int mode,
               uint32_t payload_bytes, uint32_t* out_rows, uint64_t* out_len, golp_ledger* led);
 
+/* golp_topk plus the winners' order-preserving u64 key codes (out_codes, min(k,
+ * n) entries, may be NULL): the input of golp_host_merge_topk when a key column
+ * is sharded over several contexts (B200Device(gpus=G)). */
+int golp_topk_codes(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, int mode,
+                    uint32_t payload_bytes, uint32_t* out_rows, uint64_t* out_codes, uint64_t* out_len,
+                    golp_ledger* led);
+
 /* Replaces ProxyDevice.probe (pkg/src/golp/device.py:382-436). Ships both sides
  * (build first, then the probe side in chunks that are probed as they land),
  * builds, probes, and sets *out_matches = M. When M <= out_cap the pairs are
@@ -220,6 +227,12 @@ int golp_host_hash_probe(const uint64_t* slot_bits, const uint32_t* slot_rows, u
                          uint64_t* out_matches);
 /* Phase 2: copy the M pairs of the last golp_host_hash_probe, reference order. */
 int golp_host_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m);
+/* Merge of `parts` best-first (codes, rows) lists of counts[p] entries each,
+ * stored back to back: the first k in host_topk's order (key descending, row id
+ * ascending, host.py:133-144) -> out_rows, *out_len = min(k, total). The merge
+ * step of ProxyDevice.topk (device.py:257-259) over per-GPU shard results. */
+int golp_host_merge_topk(const uint64_t* codes, const uint32_t* rows, const uint64_t* counts, int parts, uint64_t k,
+                         uint32_t* out_rows, uint64_t* out_len);
 /* Late materialization (store.materialize, store.py:184-201, and its join
  * counterpart): dst[i] = src row ids[i] (row_bytes each), multi-threaded;
  * an id >= nrows -> GOLP_ERR_INVALID. */

@@ -79,6 +79,8 @@ SIGNATURES = {
     "golp_set_profiling": (_int, [_int]),
     "golp_last_kernel_times": (_int, [C.POINTER(KernelTimes)]),
     "golp_topk": (_int, [_vp, _vp, _u64, _u64, _int, _u32, _vp, C.POINTER(_u64), C.POINTER(Ledger)]),
+    "golp_topk_codes": (_int, [_vp, _vp, _u64, _u64, _int, _u32, _vp, _vp, C.POINTER(_u64), C.POINTER(Ledger)]),
+    "golp_host_merge_topk": (_int, [_vp, _vp, _vp, _int, _u64, _vp, C.POINTER(_u64)]),
     "golp_probe": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, _int, _u32, _vp, _vp, _u64, C.POINTER(_u64),
                           C.POINTER(Ledger)]),
     "golp_probe_copy_out": (_int, [_vp, _vp, _u64, C.POINTER(Ledger)]),

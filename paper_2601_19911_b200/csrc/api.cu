@@ -1639,6 +1639,12 @@ int golp_join_probe_device(const double* d_probe_keys, const uint32_t* d_probe_r
 // ---- host buffers (E2E) -----------------------------------------------------------------
 int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, int mode, uint32_t payload_bytes,
               uint32_t* out_rows, uint64_t* out_len, golp_ledger* led) {
+  return golp_topk_codes(keys, rows, n, k, mode, payload_bytes, out_rows, nullptr, out_len, led);
+}
+
+int golp_topk_codes(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, int mode,
+                    uint32_t payload_bytes, uint32_t* out_rows, uint64_t* out_codes, uint64_t* out_len,
+                    golp_ledger* led) {
   Ctx& g = cur();
   if (k < 1) return invalid("k must be at least 1");
   uint64_t entry = 0;
@@ -1661,6 +1667,8 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
   CK(g.in_keys.ensure(n * 8));
   CK(g.in_rows.ensure(n * 4));
   CK(g.out_rows.ensure(kk * 4));
+  if (out_codes) CK(g.out_hi.ensure(kk * 8));
+  uint64_t* d_hi = out_codes ? g.out_hi.as<uint64_t>() : nullptr;  // winners' order codes (cross-shard merges)
   double* dk = g.in_keys.as<double>();
   uint32_t* dr = g.in_rows.as<uint32_t>();
   const TopkPlan p = plan_topk(n, kk);
@@ -1688,7 +1696,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     CK(cudaStreamWaitEvent(s, ev_chunk, 0));
     uint32_t* d_out = g.out_rows.as<uint32_t>();
     RET(kspan_mark(s));
-    RET(topk_device_impl(dk, dr, n, kk, d_out, nullptr, s));
+    RET(topk_device_impl(dk, dr, n, kk, d_out, d_hi, s));
     RET(kspan_mark(s));
     CK(cudaStreamSynchronize(s));  // the fused path is stream-ordered: charge its time to t_kernel
     const double t2 = wall_seconds();
@@ -1701,6 +1709,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     } else {
       RET(stage_d2h(out_rows, d_out, kk * 4));
     }
+    if (out_codes) RET(stage_d2h(out_codes, d_hi, kk * 8));
     led->t_h2d = t1 - t0;
     led->t_kernel = t2 - t1;
     led->t_d2h = wall_seconds() - t2;
@@ -1766,18 +1775,18 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
   uint32_t* d_out = g.out_rows.as<uint32_t>();
   RET(kspan_mark(s));
   if (p.direct) {
-    RET(topk_direct(dk, dr, n, kk, d_out, nullptr, s));
+    RET(topk_direct(dk, dr, n, kk, d_out, d_hi, s));
     CK(cudaStreamSynchronize(s));
   } else {
     RET(ensure_status_words());
-    RET(launch_select(cand_args(kk, p.cap, d_out, nullptr), s));
+    RET(launch_select(cand_args(kk, p.cap, d_out, d_hi), s));
     int bad = 0;
     uint64_t cands = 0;
     RET(read_topk_status(s, &bad, &cands));
     g.kt.topk_candidates = cands;
     if (bad) {
       g.kt.topk_fallback = 1;
-      RET(topk_direct(dk, dr, n, kk, d_out, nullptr, s));
+      RET(topk_direct(dk, dr, n, kk, d_out, d_hi, s));
       CK(cudaStreamSynchronize(s));
     }
   }
@@ -1793,6 +1802,7 @@ int golp_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, 
     CK(cudaStreamSynchronize(s));
     RET(stage_d2h(out_rows, d_out, kk * 4));
   }
+  if (out_codes) RET(stage_d2h(out_codes, d_hi, kk * 8));
   const double t3 = wall_seconds();
   led->t_h2d = t1 - t0;
   led->t_kernel = t2 - t1;

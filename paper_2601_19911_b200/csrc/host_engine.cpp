@@ -180,6 +180,36 @@ int golp_host_gather(const void* src, uint64_t row_bytes, uint64_t nrows, const 
   return GOLP_OK;
 }
 
+// G-way merge of best-first Top-K lists (order codes u64 + rows, as
+// golp_topk_codes returns them): the first k of all parts in host_topk's order
+// (key descending, then row id ascending; host.py:141). Shard results of
+// B200Device(gpus=G), the host side of ProxyDevice's merge (device.py:257-259).
+int golp_host_merge_topk(const uint64_t* codes, const uint32_t* rows, const uint64_t* counts, int parts, uint64_t k,
+                         uint32_t* out_rows, uint64_t* out_len) {
+  if (parts < 0 || !out_len) return invalid("bad merge arguments");
+  std::vector<uint64_t> start(parts + 1, 0), pos(parts, 0);
+  for (int p = 0; p < parts; ++p) start[p + 1] = start[p] + counts[p];
+  uint64_t o = 0;
+  while (o < k) {
+    int best = -1;
+    for (int p = 0; p < parts; ++p) {
+      if (pos[p] >= counts[p]) continue;
+      const uint64_t i = start[p] + pos[p];
+      if (best < 0) {
+        best = p;
+        continue;
+      }
+      const uint64_t j = start[best] + pos[best];
+      if (codes[i] > codes[j] || (codes[i] == codes[j] && rows[i] < rows[j])) best = p;
+    }
+    if (best < 0) break;
+    out_rows[o++] = rows[start[best] + pos[best]];
+    ++pos[best];
+  }
+  *out_len = o;
+  return GOLP_OK;
+}
+
 int golp_host_probe_copy_out(uint32_t* probe_rows, uint32_t* build_rows, uint64_t m) {
   if (m != g_probe_m) return invalid("copy_out size does not match the last host probe");
   uint64_t o = 0;

@@ -16,7 +16,8 @@ import numpy as np
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 from paper_2601_19911_b200 import (  # noqa: E402
-    B200Device, FULL_ROW, KEY_ONLY, OP_TOPK, GateConfig, calibrate_cpu_model, decide, host_topk, random_key_vector)
+    B200Device, FULL_ROW, KEY_ONLY, OP_PROBE, OP_TOPK, GateConfig, KeyVector, calibrate_cpu_model, decide,
+    host_hash_build, host_hash_probe, host_topk, random_key_vector)
 from paper_2601_19911_b200.harness import (  # noqa: E402
     WorkloadSpec, calibrate_device_profile, compute_stats, run_strategy_comparison)
 
@@ -36,6 +37,19 @@ def main(out_path):
             host_topk(kv, 100)
             ts.append(time.perf_counter() - a)
         cpu_samples.append((OP_TOPK, n, 100, sorted(ts)[1]))
+    # host-engine probes: probe side n, build n/10, keys in [0, n/5) (~0.5 matches per probe)
+    for n in (100_000, 1_000_000, 4_000_000):
+        rng = np.random.default_rng(n)
+        nb = n // 10
+        b = KeyVector(rng.integers(0, n // 5, nb).astype(np.float64), np.arange(nb, dtype=np.uint32))
+        p = KeyVector(rng.integers(0, n // 5, n).astype(np.float64), np.arange(n, dtype=np.uint32))
+        host_hash_probe(host_hash_build(b), p)
+        ts = []
+        for _ in range(3):
+            a = time.perf_counter()
+            host_hash_probe(host_hash_build(b), p)
+            ts.append(time.perf_counter() - a)
+        cpu_samples.append((OP_PROBE, n, 1, sorted(ts)[1]))
     cpu = calibrate_cpu_model(cpu_samples)
     ref_cfg = GateConfig()
     cal_cfg = GateConfig(profile=prof, cpu_model=cpu)
@@ -49,12 +63,32 @@ def main(out_path):
                 grid.append({"n": n, "k": k, "mode": mode, "reference_decision": r.path, "reference_gain_s": r.gain,
                              "calibrated_decision": c.path, "calibrated_gain_s": c.gain,
                              "c_gpu_calibrated_s": c.c_gpu_est, "c_cpu_calibrated_s": c.c_cpu_est})
+    # the M axis: probes of n keys against a build side of n/10, M (passed as k,
+    # the reference's per-probe factor in C_cpu and match count in C_gpu,
+    # gate.py:127-128 / device.py:172-175) = 1 or the expected n/2 matches
+    probe_grid = []
+    for n in (1_000, 10_000, 20_000, 100_000, 1_000_000, 10_000_000, 100_000_000, 1_000_000_000):
+        for m in (1, max(1, n // 2)):
+            for mode in (KEY_ONLY, FULL_ROW):
+                pb = 188 if mode == FULL_ROW else None
+                r = decide(GateConfig(mode=mode), OP_PROBE, n, m, pb, build_n=n // 10)
+                c = decide(GateConfig(mode=mode, profile=prof, cpu_model=cpu), OP_PROBE, n, m, pb, build_n=n // 10)
+                probe_grid.append({"n_probe": n, "n_build": n // 10, "m": m, "mode": mode,
+                                   "reference_decision": r.path, "reference_gain_s": r.gain,
+                                   "calibrated_decision": c.path, "calibrated_gain_s": c.gain,
+                                   "c_gpu_calibrated_s": c.c_gpu_est, "c_cpu_calibrated_s": c.c_cpu_est})
     strat = {}
+    # crit 7's exact stream (pkg/tests/test_acceptance.py:252-270): 500 queries,
+    # 80/20 over n in {1e4, 1e6}, seed 3, 188-byte payloads; three runs each
+    spec = WorkloadSpec(n_grid=(10_000, 1_000_000), repeats=250, mix=(0.8, 0.2), seed=3)
+    tables = {}
     for label, cfg in (("reference_constants", ref_cfg), ("calibrated", cal_cfg)):
-        spec = WorkloadSpec(n_grid=(10_000, 1_000_000), repeats=100, mix=(0.8, 0.2), seed=3, payload_bytes=16)
-        runs = run_strategy_comparison(spec, cfg, device=dev)
-        strat[label] = {r.strategy: {**{k: getattr(compute_stats(r.all_samples()), k) for k in ("median", "p95", "p99")},
-                                     "offload_rate": r.offload_rate} for r in runs}
+        strat[label] = []
+        for _ in range(3):
+            runs = run_strategy_comparison(spec, cfg, device=dev, tables=tables)
+            strat[label].append({r.strategy: {**{k: getattr(compute_stats(r.all_samples()), k)
+                                                 for k in ("median", "p95", "p99")},
+                                              "offload_rate": r.offload_rate} for r in runs})
     # the paper's key-only vs full-row experiment on the B200:
     # Top-K K=100, payload 188 B; E2E full-row = h2d+kernel+d2h, key-only = whole
     # ledger incl. late materialization (run_payload_comparison semantics)
@@ -70,7 +104,7 @@ def main(out_path):
                    next(r.transfer_s for r in pay.payload_rows if r.n == n and r.mode == KEY_ONLY)
                    for n in (1_000_000, 3_000_000, 10_000_000)}}
     out = {"profile_b200": prof.to_json_dict(), "cpu_model_host_engine": cpu.to_json_dict(),
-           "decisions": grid, "strategy_80_20_stream": strat, "key_only_vs_full_row": payload,
+           "decisions": grid, "probe_decisions": probe_grid, "strategy_80_20_stream": strat, "key_only_vs_full_row": payload,
            "wall_s": time.time() - t0}
     Path(out_path).write_text(json.dumps(out, indent=1))
     print(json.dumps({"profile": out["profile_b200"], "strategies": strat,
