@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(1024) join_big_groups_kernel(const Slot* __res
 #define GOLP_WARP_ITEMS 2
 #endif
 #ifndef GOLP_PROBE_MINB
-#define GOLP_PROBE_MINB 6
+#define GOLP_PROBE_MINB 5
 #endif
 constexpr int kWarpItems = GOLP_WARP_ITEMS;
 static_assert(kWarpItems % 2 == 0, "keys are loaded as 16-byte pairs");
@@ -773,9 +773,10 @@ constexpr unsigned kProbeWarps = kProbeThreads / 32;
 
 // Appends one warp tile's hits (probe row, slot.off, slot.cnt) to the warp's
 // scratch run in probe order; returns the tile's pair count.
-__device__ __forceinline__ uint64_t warp_append_hits(unsigned lane, uint64_t first, const uint32_t* off,
-                                                     const uint32_t* cnt, const uint32_t* __restrict__ prows,
-                                                     const MatchScratch& sc, uint64_t& cursor) {
+// prow: the probe rows of this lane's kWarpItems probes, loaded with the keys
+// (a load issued only after the lookups would add a dependent round trip).
+__device__ __forceinline__ uint64_t warp_append_hits(unsigned lane, const uint32_t* off, const uint32_t* cnt,
+                                                     const uint32_t* prow, const MatchScratch& sc, uint64_t& cursor) {
   uint32_t nm = 0;
   uint64_t npr = 0;
 #pragma unroll
@@ -794,14 +795,11 @@ __device__ __forceinline__ uint64_t warp_append_hits(unsigned lane, uint64_t fir
   for (int o = 16; o > 0; o >>= 1) tpairs += __shfl_xor_sync(0xFFFFFFFFu, tpairs, o);
   const uint32_t tmatch = __shfl_sync(0xFFFFFFFFu, incl, 31);
   if (nm) {
-    uint32_t r[kWarpItems];
-#pragma unroll
-    for (int j = 0; j < kWarpItems; ++j) r[j] = cnt[j] ? __ldg(prows + first + j) : 0u;
     uint64_t o = cursor + (incl - nm);
 #pragma unroll
     for (int j = 0; j < kWarpItems; ++j) {
       if (cnt[j]) {
-        sc.prow[o] = r[j];
+        sc.prow[o] = prow[j];
         sc.off[o] = off[j];
         sc.cnt[o] = cnt[j];
         ++o;
@@ -841,7 +839,7 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_ker
   uint64_t pairs_total = 0;
   for (uint64_t wt = lo; wt < hi; ++wt) {
     const uint64_t first = wt * kWarpTile + lane * kWarpItems;
-    uint32_t off[kWarpItems], cnt[kWarpItems];
+    uint32_t off[kWarpItems], cnt[kWarpItems], prow[kWarpItems];
     double k[kWarpItems];
     if (first + kWarpItems <= np && (((uintptr_t)(pkeys + first) & 15) == 0)) {
 #pragma unroll
@@ -854,6 +852,10 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_ker
 #pragma unroll
       for (int j = 0; j < kWarpItems; ++j) k[j] = first + j < np ? pkeys[first + j] : 0.0;
     }
+    // the probe rows go out with the keys (a load after the lookups would add a
+    // dependent round trip to every tile with a hit)
+#pragma unroll
+    for (int j = 0; j < kWarpItems; ++j) prow[j] = first + j < np ? __ldcs(prows + first + j) : 0u;
     uint64_t bits[kWarpItems];
     uint32_t h[kWarpItems];
     unsigned pending = 0;
@@ -880,7 +882,7 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_ker
       }
       home = false;
     }
-    pairs_total += warp_append_hits(lane, first, off, cnt, prows, sc, cursor);
+    pairs_total += warp_append_hits(lane, off, cnt, prow, sc, cursor);
   }
   finish_match_block(lane, warp, gw, lo, cursor, pairs_total, sc, s_w, bpart);
 }
@@ -1024,16 +1026,25 @@ __global__ void __launch_bounds__(kProbeThreads) join_match_runs_kernel(
   const uint64_t lo = gw * kRunWarpTiles, hi = lo + kRunWarpTiles < nwt ? lo + kRunWarpTiles : nwt;
   uint64_t cursor = lo * kWarpTile;
   uint64_t pairs_total = 0;
+  uint32_t nrow[kWarpItems];  // the next warp tile's probe rows, loaded one tile ahead
+#pragma unroll
+  for (int j = 0; j < kWarpItems; ++j) {
+    const uint64_t i = lo * kWarpTile + lane * kWarpItems + j;
+    nrow[j] = lo < hi && i < np ? __ldcs(prows + i) : 0u;
+  }
   for (uint64_t wt = lo; wt < hi; ++wt) {
     const uint64_t first = wt * kWarpTile + lane * kWarpItems;
-    uint32_t off[kWarpItems], cnt[kWarpItems];
+    uint32_t off[kWarpItems], cnt[kWarpItems], prow[kWarpItems];
 #pragma unroll
     for (int j = 0; j < kWarpItems; ++j) {
       const uint64_t v = first + j < np ? s_res[first + j - t0] : 0ull;
       off[j] = (uint32_t)v;
       cnt[j] = (uint32_t)(v >> 32);
+      prow[j] = nrow[j];
+      const uint64_t i = first + kWarpTile + j;
+      nrow[j] = wt + 1 < hi && i < np ? __ldcs(prows + i) : 0u;
     }
-    pairs_total += warp_append_hits(lane, first, off, cnt, prows, sc, cursor);
+    pairs_total += warp_append_hits(lane, off, cnt, prow, sc, cursor);
   }
   finish_match_block(lane, warp, gw, lo, cursor, pairs_total, sc, s_w, bpart);
 }
