@@ -23,7 +23,7 @@ from .device import (DEFAULT_MODELED_PROFILE, FULL_ROW, KEY_ONLY, OP_PROBE, OP_T
 from .errors import StrategyMismatchError
 from .gate import DEFAULT_CPU_MODEL, DEVICE, HOST, OP_FULL_SORT, GateConfig, estimate_cpu_cost, execute_gated, execute_path
 from .host import host_full_sort, host_topk, mix64
-from .store import DEFAULT_PAYLOAD_BYTES, ColumnTable, generate_table, random_key_vector
+from .store import DEFAULT_MEMORY_BUDGET, DEFAULT_PAYLOAD_BYTES, ColumnTable, generate_table, random_key_vector
 
 HOST_ONLY = "host_only"
 DEVICE_ALWAYS = "device_always"
@@ -46,6 +46,8 @@ class WorkloadSpec:
     payload_bytes: int = DEFAULT_PAYLOAD_BYTES
     mix: Optional[tuple] = None
     seed: int = 0
+    # tables' memory budget (store.generate_table); None: no cap (large-N key-only runs)
+    memory_budget: Optional[int] = DEFAULT_MEMORY_BUDGET
 
     def __post_init__(self) -> None:
         grid = tuple(int(n) for n in self.n_grid)
@@ -200,7 +202,8 @@ def run_strategy_comparison(spec: WorkloadSpec, config: GateConfig, device=None,
     tables = {} if tables is None else tables
     for n in spec.n_grid:
         if n not in tables:
-            tables[n] = generate_table(n, spec.payload_bytes, seed=table_seed(spec.seed, n))
+            tables[n] = generate_table(n, spec.payload_bytes, seed=table_seed(spec.seed, n),
+                                       memory_budget=spec.memory_budget)
     fingerprints: dict = {}
     first: dict = {}
 

@@ -277,3 +277,20 @@ def test_materialize_joins_on_the_query_path_cpu():
         assert np.array_equal(res.probe.keys, res.build.keys)
         assert np.array_equal(res.probe.payloads, pt.payload_column[res.probe.row_ids])
         assert np.array_equal(res.build.payloads, bt.payload_column[res.build.row_ids])
+
+
+def test_cli_bench_modeled_writes_golp_style_outputs(tmp_path):
+    """`cli bench` (golp bench's shape, pkg/src/golp/cli.py:183-237) on the modeled backend."""
+    import json
+
+    from paper_2601_19911_b200 import cli
+
+    cfg = tmp_path / "cfg.json"
+    cfg.write_text(json.dumps({"workload": {"n_grid": [1_000, 10_000, 100_000], "repeats": 2, "payload_bytes": 16},
+                               "gpus": 1}))
+    assert cli.main(["bench", "--config", str(cfg), "--backend", "modeled", "--out", str(tmp_path / "out")]) == 0
+    summary = json.loads((tmp_path / "out" / "summary.json").read_text())
+    assert summary["backend"] == "modeled" and set(summary["strategies"]) == {"host_only", "device_always", "gated"}
+    for f in ("scaling.csv", "payload.csv", "transfer.csv", "e2e.csv", "strategies.csv"):
+        assert (tmp_path / "out" / f).read_text().count("\n") > 1
+    assert cli.main(["bench", "--backend", "modeled", "--gpus", "0", "--out", str(tmp_path / "o2")]) == 2

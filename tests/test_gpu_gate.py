@@ -120,3 +120,18 @@ def test_criterion_07_stream_on_b200(b200):
         assert g.median < h.median and g.median < d.median
         assert g.p95 <= h.p95 and g.p99 <= h.p99
         assert g.p95 <= 1.10 * d.p95 and g.p99 <= 1.10 * d.p99
+
+
+def test_cli_bench_on_the_b200(tmp_path, b200):
+    """`cli bench --backend b200`: calibrated gate, B200 rows in every output."""
+    import json
+
+    from paper_2601_19911_b200 import cli
+
+    cfg = tmp_path / "cfg.json"
+    cfg.write_text(json.dumps({"workload": {"n_grid": [10_000, 200_000, 1_000_000], "repeats": 3,
+                                            "payload_bytes": 16}}))
+    assert cli.main(["bench", "--config", str(cfg), "--backend", "b200", "--out", str(tmp_path / "out")]) == 0
+    summary = json.loads((tmp_path / "out" / "summary.json").read_text())
+    assert summary["backend"] == "b200" and summary["gate"]["profile"]["kernel_rate_topk"] > 1e-12
+    assert "topk@b200" in (tmp_path / "out" / "scaling.csv").read_text()
