@@ -7,6 +7,7 @@
 //   host_topk        pkg/src/golp/host.py:133-144  (k largest, ties by row id)
 //   host_hash_build  pkg/src/golp/host.py:147-165  (KeyHashTable slot layout)
 //   host_hash_probe  pkg/src/golp/host.py:168-188  (probe order, then chain order)
+#include <cstdlib>
 #include <algorithm>
 #include <memory>
 
@@ -160,7 +161,10 @@ int golp_host_gather(const void* src, uint64_t row_bytes, uint64_t nrows, const 
     }
     // Rows are random in a table far larger than the caches: prefetch the rows
     // kAhead ids ahead (every cache line of each) so that many misses overlap.
-    constexpr uint64_t kAhead = 16;
+    static const uint64_t kAhead = [] {
+      const char* v = std::getenv("GOLP_GATHER_PREFETCH");
+      return v ? (uint64_t)std::strtoull(v, nullptr, 10) : (uint64_t)32;
+    }();
     auto prefetch_row = [&](uint64_t i) {
       const uint32_t r = ids[i];
       if (r >= nrows) return;
@@ -170,7 +174,7 @@ int golp_host_gather(const void* src, uint64_t row_bytes, uint64_t nrows, const 
     };
     for (uint64_t i = lo; i < std::min(hi, lo + kAhead); ++i) prefetch_row(i);
     for (uint64_t i = lo; i < hi; ++i) {
-      if (i + kAhead < hi) prefetch_row(i + kAhead);
+      if (kAhead && i + kAhead < hi) prefetch_row(i + kAhead);
       const uint32_t r = ids[i];
       if (r >= nrows) { bad = true; return; }
       std::memcpy(d + i * row_bytes, s + (uint64_t)r * row_bytes, row_bytes);
