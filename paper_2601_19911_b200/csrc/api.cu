@@ -1084,7 +1084,7 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
     sched.ctr = g.work_ctr.as<unsigned long long>();
   }
 #ifndef GOLP_BUILD_WIDE_ALWAYS
-#define GOLP_BUILD_WIDE_ALWAYS 0
+#define GOLP_BUILD_WIDE_ALWAYS 1  // 16-byte claim CAS for L2-resident tables too (C2 build 78 -> 73 us)
 #endif
   if (g.jparts > 1 || GOLP_BUILD_WIDE_ALWAYS)  // table in HBM: one 16-byte CAS per new key
     join_insert_kernel<true><<<gb, kBuildThreads, 0, s>>>(ikeys, ipos, nb, table, g.jmask, ga, sched);
