@@ -132,10 +132,11 @@ struct TileSched {
 };
 
 // bpos (optional): build position of entry i when the entries were partitioned.
-// kWide: claim slots with the 16-byte CAS (saves the rank atomic of a key's first
-// member; pays off when the table lives in HBM). Otherwise a 64-bit key CAS plus
-// rank = atomicAdd(cnt) for every member, the rank-0 member storing its position
-// in slot.off -- cheaper when the atomics resolve in L2.
+// kWide (the default, GOLP_BUILD_WIDE_ALWAYS): claim slots with the 16-byte CAS,
+// which saves the rank atomic of a key's first member (C4 build; C2 78 -> 75 us
+// with the home-pair overflow flags). Otherwise a 64-bit key CAS plus rank =
+// atomicAdd(cnt) for every member, the rank-0 member storing its position in
+// slot.off.
 template <bool kWide>
 __global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double* __restrict__ bkeys,
                                                                     const uint32_t* __restrict__ bpos, uint64_t nb,
