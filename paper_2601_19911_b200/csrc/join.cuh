@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_
       table[h].off = (uint32_t)(h * kInline);
     }
     const uint32_t need = cnt > kInline ? cnt : 0u;  // big group: reserve its CSR range
+    if (!__ballot_sync(0xFFFFFFFFu, need != 0)) continue;  // (almost every warp of slots)
     unsigned long long incl = need;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
