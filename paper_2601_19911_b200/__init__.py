@@ -76,10 +76,12 @@ from .store import (
     full_row_bytes,
     generate_table,
     key_only_bytes,
+    load_table,
     materialize,
     materialize_join,
     random_key_vector,
     random_keys,
+    save_table,
 )
 
 __version__ = "0.1.0"

@@ -294,3 +294,36 @@ def test_cli_bench_modeled_writes_golp_style_outputs(tmp_path):
     for f in ("scaling.csv", "payload.csv", "transfer.csv", "e2e.csv", "strategies.csv"):
         assert (tmp_path / "out" / f).read_text().count("\n") > 1
     assert cli.main(["bench", "--backend", "modeled", "--gpus", "0", "--out", str(tmp_path / "o2")]) == 2
+
+
+def test_table_dump_round_trip_and_reference_format(tmp_path):
+    """save_table / load_table in the reference's dump format (store.py:214-244):
+    byte-identical files, and each side loads the other's dumps."""
+    import sys
+    from pathlib import Path
+
+    from paper_2601_19911_b200 import store
+
+    t = store.generate_table(5_000, 12, seed=9)
+    ours = tmp_path / "ours.golp"
+    store.save_table(t, ours)
+    for mapped in (True, False):
+        back = store.load_table(ours, mapped=mapped)
+        assert back.seed == t.seed and np.array_equal(back.key_column, t.key_column)
+        assert np.array_equal(back.payload_column, t.payload_column)
+        assert not back.key_column.flags.writeable
+    bad = tmp_path / "bad.golp"
+    bad.write_bytes(ours.read_bytes()[:-1])
+    with pytest.raises(ValueError):
+        store.load_table(bad)
+    ref = Path(__file__).resolve().parents[1] / "baseline" / "_ref"
+    if not (ref / "golp").exists():
+        pytest.skip("reference golp not installed (baseline/install_reference.sh)")
+    sys.path.insert(0, str(ref))
+    import golp.store as gs
+
+    theirs = tmp_path / "theirs.golp"
+    gs.save_table(gs.generate_table(5_000, 12, seed=9), theirs)
+    assert theirs.read_bytes() == ours.read_bytes()
+    g = gs.load_table(ours)
+    assert np.array_equal(g.key_column, t.key_column) and np.array_equal(g.payload_column, t.payload_column)
