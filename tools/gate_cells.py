@@ -4,7 +4,7 @@ materialize, gate.execute_path semantics, pkg/src/golp/gate.py:167-233) for
 CPU-only (the host engine), always-on offload (B200Device) and the Risky Gate
 (execute_gated with the calibrated profile / CPU model), plus the gate's choice.
 
-    python tools/gate_cells.py [out.json] [--max-n N]
+    python tools/gate_cells.py [out.json] [--max-n N]      (N up to 1e9; full-row cells to 1e7)
 
 The DeviceProfile is calibrated from B200 ledgers and the CpuCostModel from
 host-engine timings in the same run (tools/gate_sweep.py does the same); the
@@ -36,7 +36,7 @@ IDLE_S = 0.002
 
 
 def repeats_for(n):
-    return 25 if n <= 100_000 else (11 if n <= 1_000_000 else (5 if n <= 10_000_000 else 3))
+    return 25 if n <= 100_000 else (11 if n <= 1_000_000 else (5 if n <= 10_000_000 else (3 if n <= 100_000_000 else 2)))
 
 
 def stats(ts):
@@ -132,7 +132,7 @@ def main(out_path, max_n):
     wall = sorted(execute_path(small, OP_TOPK, 10, cfg0, dev, DEVICE)[1] for _ in range(9))[4]
     margin_k = max(0.0, wall - execute_gated(small, OP_TOPK, 10, cfg0, dev)[1].c_gpu_est)
     cells = []
-    ns = [n for n in (1_000, 10_000, 100_000, 1_000_000, 10_000_000, 100_000_000) if n <= max_n]
+    ns = [n for n in (1_000, 10_000, 100_000, 1_000_000, 10_000_000, 100_000_000, 1_000_000_000) if n <= max_n]
     for n in ns:
         for mode in (KEY_ONLY, FULL_ROW):
             if mode == FULL_ROW and n > 10_000_000:
@@ -181,7 +181,7 @@ def _time(fn, reps=3, idle_s=0.0):
 
 if __name__ == "__main__":
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    max_n = 100_000_000
+    max_n = 1_000_000_000
     if "--max-n" in sys.argv:
         max_n = int(float(sys.argv[sys.argv.index("--max-n") + 1]))
     main(args[0] if args else "gpurun_out/gate_cells.json", max_n)
