@@ -8,6 +8,8 @@ print("cpu", d["cpu_model_host_engine"])
 
 
 def f(s):
+    if "p50" not in s:  # a host path the reference refuses (CapacityError)
+        return f"{'refused (' + s.get('error', '?')[:13] + ')':>29s}"
     return f"{s['p50'] * 1e3:9.3f}/{s['p95'] * 1e3:9.3f}/{s['p99'] * 1e3:9.3f}"
 
 
