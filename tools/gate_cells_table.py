@@ -32,7 +32,8 @@ def summary(tag, choice_key, prefix):
     cells = d["cells"]
     if choice_key not in cells[0]:
         return
-    right = sum((c[choice_key] == "device") == (c["always_on"]["p50"] < c["cpu_only"]["p50"]) for c in cells)
+    right = sum((c[choice_key] == "device") == (c["always_on"]["p50"] < c["cpu_only"].get("p50", float("inf")))
+                for c in cells)
     le95 = sum(c[f"{prefix}p95_over_best_fixed"] <= 1.0 for c in cells)
     w5 = sum(c[f"{prefix}p95_over_best_fixed"] <= 1.05 for c in cells)
     print(f"{tag}: faster path chosen in {right}/{len(cells)} cells; P95 <= best fixed in {le95}, within 5% in {w5}")
