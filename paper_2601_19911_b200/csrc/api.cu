@@ -194,7 +194,11 @@ int default_handle(int device) {
 Ctx& cur() {
   if (!t_cur) {
     const int h = default_handle(device_of_thread());
-    t_cur = g_ctx[h >= 0 ? h : 0];
+    // no context slot left (or a device index past kMaxContexts): an unusable
+    // context whose initialization reports the error
+    static Ctx unusable;
+    unusable.device = kMaxContexts;
+    t_cur = h >= 0 ? g_ctx[h] : &unusable;
   }
   return *t_cur;
 }
@@ -1378,6 +1382,9 @@ void release_context(Ctx& g) {
   g.per_sm.clear();
   for (cudaEvent_t e : g.trace_ev) cudaEventDestroy(e);
   g.trace_ev.clear();
+  for (cudaEvent_t e : g.kspan_ev) cudaEventDestroy(e);
+  g.kspan_ev.clear();
+  g.kspan_n = 0;
   g.ready = false;
 }
 
