@@ -75,3 +75,39 @@ def test_host_engine_probe_matches_reference(case):
     assert res.probe_rows.tolist() == case["exp_p"].tolist()
     assert res.build_rows.tolist() == case["exp_b"].tolist()
     assert res.probe_count == len(case["pkeys"])
+
+
+@pytest.mark.parametrize("parts,k", [(1, 10), (3, 100), (8, 5_000), (5, 1)])
+def test_host_merge_topk_of_shard_lists(parts, k):
+    """golp_host_merge_topk (the merge of B200Device(gpus=G)'s per-GPU top-K lists):
+    the first k of all lists in host_topk's order -- order code descending, row
+    ascending on ties (host.py:141) -- from best-first inputs with ties across lists."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(parts * 1000 + k)
+    n = 40_000
+    keys = rng.integers(-50, 50, n).astype(np.float64)  # heavy ties, negatives, zeros
+    rows = rng.permutation(n).astype(np.uint32)
+    bounds = np.linspace(0, n, parts + 1).astype(np.int64)
+    codes_l, rows_l, counts = [], [], []
+    key_of_row = np.empty(n, dtype=np.float64)
+    key_of_row[rows] = keys
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        r = oracle.topk(keys[a:b], rows[a:b], k)  # a shard's best-first list
+        kk = key_of_row[r]
+        bits = (kk + 0.0).view(np.uint64)
+        codes = np.where(bits >> np.uint64(63), ~bits, bits | np.uint64(1 << 63))  # ord(key)
+        codes_l.append(codes)
+        rows_l.append(r)
+        counts.append(len(r))
+    codes = np.ascontiguousarray(np.concatenate(codes_l), dtype=np.uint64)
+    cand = np.ascontiguousarray(np.concatenate(rows_l), dtype=np.uint32)
+    cnt = np.asarray(counts, dtype=np.uint64)
+    out = np.empty(k, dtype=np.uint32)
+    got = C.c_uint64(0)
+    lib = _native.load()
+    assert lib.golp_host_merge_topk(_native.ptr(codes), _native.ptr(cand), _native.ptr(cnt), parts, k,
+                                    _native.ptr(out), C.byref(got)) == _native.GOLP_OK
+    want = oracle.topk(keys, rows, k)
+    assert got.value == len(want)
+    np.testing.assert_array_equal(out[: got.value], want)
