@@ -777,6 +777,8 @@ constexpr unsigned kProbeWarps = kProbeThreads / 32;
 // scratch run in probe order; returns the tile's pair count.
 // prow: the probe rows of this lane's kWarpItems probes, loaded with the keys
 // (a load issued only after the lookups would add a dependent round trip).
+// Returns this LANE's pair count of the tile (the warp total is reduced once,
+// at the end of the warp's run).
 __device__ __forceinline__ uint64_t warp_append_hits(unsigned lane, const uint32_t* off, const uint32_t* cnt,
                                                      const uint32_t* prow, const MatchScratch& sc, uint64_t& cursor) {
   uint32_t nm = 0;
@@ -786,18 +788,17 @@ __device__ __forceinline__ uint64_t warp_append_hits(unsigned lane, const uint32
     nm += cnt[j] != 0;
     npr += cnt[j];
   }
-  uint32_t incl = nm;
+  // hits of the lanes before this one, and of the tile: one ballot per hit count
+  const unsigned lt = (1u << lane) - 1u;
+  uint32_t excl = 0, tmatch = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if ((int)lane >= o) incl += v;
+  for (int t = 1; t <= kWarpItems; ++t) {
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, nm >= (uint32_t)t);
+    excl += __popc(b & lt);
+    tmatch += __popc(b);
   }
-  uint64_t tpairs = npr;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) tpairs += __shfl_xor_sync(0xFFFFFFFFu, tpairs, o);
-  const uint32_t tmatch = __shfl_sync(0xFFFFFFFFu, incl, 31);
   if (nm) {
-    uint64_t o = cursor + (incl - nm);
+    uint64_t o = cursor + excl;
 #pragma unroll
     for (int j = 0; j < kWarpItems; ++j) {
       if (cnt[j]) {
@@ -809,13 +810,15 @@ __device__ __forceinline__ uint64_t warp_append_hits(unsigned lane, const uint32
     }
   }
   cursor += tmatch;
-  return tpairs;
+  return npr;
 }
 
 // Per-warp totals -> scratch counters and the block's pair total.
 __device__ __forceinline__ void finish_match_block(unsigned lane, unsigned warp, uint64_t gw, uint64_t lo,
                                                    uint64_t cursor, uint64_t pairs_total, const MatchScratch& sc,
                                                    unsigned long long* s_w, unsigned long long* __restrict__ bpart) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pairs_total += __shfl_xor_sync(0xFFFFFFFFu, pairs_total, o);  // lanes -> warp
   if (lane == 0) {
     sc.wentries[gw] = (uint32_t)(cursor - lo * kWarpTile);
     sc.wpairs[gw] = pairs_total;
@@ -1114,11 +1117,22 @@ __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch s
     }
 #pragma unroll
     for (int q = 0; q < kBatch; ++q) {
-      uint64_t incl = c[q];
+      uint64_t incl;
+      if (__any_sync(0xFFFFFFFFu, c[q] >= (1u << 26))) {  // huge key groups: 64-bit scan
+        incl = c[q];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if ((int)lane >= o) incl += v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint64_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if ((int)lane >= o) incl += v;
+        }
+      } else {  // 32 counts below 2^26 cannot overflow a 32-bit scan
+        uint32_t i32 = c[q];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, i32, o);
+          if ((int)lane >= o) i32 += v;
+        }
+        incl = i32;
       }
       unsigned long long g = run + (incl - c[q]);
       if (c[q] == 1) {  // singleton: slot.off is its row, or its position past the first row id
