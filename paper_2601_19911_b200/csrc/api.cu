@@ -113,7 +113,7 @@ struct Ctx {
 
   DevBuf ctl, cand_hi, cand_lo, w_hi, w_lo, out_rows, out_hi, samples;
   DevBuf table, rows_arr, ovf, big_list, jcount, wcount, partial, totals, totals2;
-  DevBuf sc_prow, sc_off, sc_cnt;
+  DevBuf sc_prow, sc_oc;
   DevBuf part_keys, part_pos, part_cnt, part_cur, run_base, run_len, res_part, work_ctr;
   DevBuf pairs_p, pairs_b;
   DevBuf rows_flag;  // build row column is a dense run (join_build_impl)
@@ -1135,14 +1135,12 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
   const uint64_t nwt_max = (sub + kWarpTile - 1) / kWarpTile;
   const uint64_t nwarps_max = (uint64_t)g.sms * GOLP_PROBE_MINB * kProbeWarps;
   CK(g.sc_prow.ensure(nwt_max * kWarpTile * 4));
-  CK(g.sc_off.ensure(nwt_max * kWarpTile * 4));
-  CK(g.sc_cnt.ensure(nwt_max * kWarpTile * 4));
+  CK(g.sc_oc.ensure(nwt_max * kWarpTile * 8));
   CK(g.wcount.ensure((std::max(nwt_max, nwarps_max) + kProbeWarps) * 12));
   CK(g.totals2.ensure(16));
   MatchScratch sc;
   sc.prow = g.sc_prow.as<uint32_t>();
-  sc.off = g.sc_off.as<uint32_t>();
-  sc.cnt = g.sc_cnt.as<uint32_t>();
+  sc.oc = g.sc_oc.as<uint64_t>();
   unsigned long long* tmp = g.totals2.as<unsigned long long>();
   const uint64_t span = part_probe ? kSpan : np;
   uint64_t ci = 0;  // running sub-chunk index (pair-offset chaining)
@@ -1336,7 +1334,7 @@ void release_context(Ctx& g) {
   g.pool.stop();
   DevBuf* bufs[] = {&g.ctl, &g.cand_hi, &g.cand_lo, &g.w_hi, &g.w_lo, &g.out_rows, &g.out_hi, &g.samples,
                     &g.table, &g.rows_arr, &g.ovf, &g.big_list, &g.jcount,
-                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_off, &g.sc_cnt, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.srt_hist, &g.srt_k0, &g.srt_k1, &g.srt_r0, &g.srt_r1, &g.srt_status, &g.srt_base, &g.in_keys, &g.in_rows,
+                    &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_oc, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.srt_hist, &g.srt_k0, &g.srt_k1, &g.srt_r0, &g.srt_r1, &g.srt_status, &g.srt_base, &g.in_keys, &g.in_rows,
                     &g.in_bkeys, &g.in_brows, &g.in_payload, &g.rows_flag, &g.row_base};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < kSlots; ++i) {

@@ -760,13 +760,12 @@ __device__ __forceinline__ int check_pair(const ulonglong4& sl, uint64_t bits, u
   return -1;
 }
 
-// Scratch entries are SoA {probe row, slot.off, slot.cnt}. Each warp owns a
+// Scratch entries are SoA {u32 probe row, u64 slot.off | slot.cnt << 32}. Each warp owns a
 // contiguous run of warp tiles and appends its hits contiguously (in probe
 // order) starting at its first tile's slot, so emit is a streaming copy.
 struct MatchScratch {
   uint32_t* prow;
-  uint32_t* off;
-  uint32_t* cnt;
+  uint64_t* oc;  // slot.off | slot.cnt << 32 (one 8-byte store / load per hit)
   uint32_t* wentries;            // per global warp: entries written
   unsigned long long* wpairs;    // per global warp: pairs produced (sum of cnt; 64-bit, big key groups)
 };
@@ -803,8 +802,7 @@ __device__ __forceinline__ uint64_t warp_append_hits(unsigned lane, const uint32
     for (int j = 0; j < kWarpItems; ++j) {
       if (cnt[j]) {
         sc.prow[o] = prow[j];
-        sc.off[o] = off[j];
-        sc.cnt[o] = cnt[j];
+        sc.oc[o] = ((uint64_t)cnt[j] << 32) | off[j];
         ++o;
       }
     }
@@ -1100,7 +1098,10 @@ __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch s
   const uint32_t rb = __ldg(row_base);
   const uint64_t e0 = lo * kWarpTile;
   const uint32_t ne = sc.wentries[gw];
-  constexpr int kBatch = 4;  // 4 x 32 entries in flight per warp iteration
+#ifndef GOLP_EMIT_BATCH
+#define GOLP_EMIT_BATCH 4
+#endif
+  constexpr int kBatch = GOLP_EMIT_BATCH;  // kBatch x 32 entries in flight per warp iteration
   for (uint32_t i0 = 0; i0 < ne; i0 += 32 * kBatch) {
     uint32_t c[kBatch], pr[kBatch], of[kBatch];
 #pragma unroll
@@ -1110,9 +1111,11 @@ __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch s
       pr[q] = 0;
       of[q] = 0;
       if (i < ne) {
-        c[q] = __ldcs(sc.cnt + e0 + i);
+        const uint64_t v = __ldcs(reinterpret_cast<const unsigned long long*>(sc.oc) + e0 + i);
+        c[q] = (uint32_t)(v >> 32);
+        of[q] = (uint32_t)v;
         pr[q] = __ldcs(sc.prow + e0 + i);
-        of[q] = __ldcs(sc.off + e0 + i);
+
       }
     }
 #pragma unroll
