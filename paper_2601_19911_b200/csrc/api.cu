@@ -1818,6 +1818,9 @@ int golp_topk_codes(const double* keys, const uint32_t* rows, uint64_t n, uint64
 #ifndef GOLP_TAIL_SPLIT
 #define GOLP_TAIL_SPLIT 4
 #endif
+#ifndef GOLP_H2D_AHEAD
+#define GOLP_H2D_AHEAD 2
+#endif
 int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb, const double* probe_keys,
                const uint32_t* probe_rows, uint64_t np, int mode, uint32_t payload_bytes, uint32_t* out_probe_rows,
                uint32_t* out_build_rows, uint64_t out_cap, uint64_t* out_matches, golp_ledger* led) {
@@ -1973,11 +1976,12 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
       return GOLP_OK;
     }
     for (uint64_t c = 0; c < nchunks; ++c) {
-      // Keep at most two chunks of uploads in flight: copies are serviced in
-      // submission order, so pair downloads queued in between can overlap them.
-      if (c >= 2) {
+      // Keep at most GOLP_H2D_AHEAD chunks of uploads in flight: copies are
+      // serviced in submission order, so pair downloads queued in between can
+      // overlap them.
+      if (c >= GOLP_H2D_AHEAD) {
         while (true) {
-          const cudaError_t q = cudaEventQuery(g.h2d_ev[c - 2]);
+          const cudaError_t q = cudaEventQuery(g.h2d_ev[c - GOLP_H2D_AHEAD]);
           if (q == cudaSuccess) break;
           if (q != cudaErrorNotReady) CK(q);
           RET(stream_ready(false));

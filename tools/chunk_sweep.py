@@ -28,9 +28,9 @@ def run(dev, fn, warm=5, steps=20):
 
 
 def main(mibs):
-    bk, br, pk, pr = join_data(WORKLOADS["join_c2"], 0)
+    bk, br, pk, pr = join_data(WORKLOADS["join_c2"])
     kb, kp = KeyVector(bk, br), KeyVector(pk, pr)
-    keys, rows = topk_data(WORKLOADS["topk_c1"], 0)[:2]
+    keys, rows = topk_data(WORKLOADS["topk_c1"])
     kv = KeyVector(keys, rows)
     for mib in mibs:
         dev = B200Device(pinned_chunk_bytes=int(mib * (1 << 20)))
