@@ -80,6 +80,13 @@ constexpr uint32_t kInline = 4;
 // reader of cnt masks it.
 constexpr uint32_t kOverflowBit = 1u << 31;
 constexpr uint32_t kCntMask = kOverflowBit - 1u;
+// Two-member groups whose second row fits 30 bits live in the slot itself:
+// off = first row, cnt word = kPair2Bit | second row (probe/emit read no side
+// array for them; most groups have two members). Other counts stay below 2^30.
+constexpr uint32_t kPair2Bit = 1u << 30;
+constexpr uint32_t kPair2Row = kPair2Bit - 1u;
+// Members of a slot's key from its cnt word (overflow flag already masked off).
+__host__ __device__ __forceinline__ uint32_t slot_members(uint32_t cw) { return (cw & kPair2Bit) ? 2u : cw; }
 constexpr uint32_t kGroupTile = 16384;  // big groups up to this size sorted in shared memory (64 KB)
 
 __global__ void join_init_table_kernel(Slot* __restrict__ table, uint64_t cap) {
@@ -276,11 +283,12 @@ __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t wb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; wb < cap; wb += stride) {
     const uint64_t h = wb + lane;
-    uint32_t cnt = 0, first = 0;  // first: rank-0 position, stored inline by the claiming CAS
+    uint32_t cnt = 0, first = 0, oflag = 0;  // first: rank-0 position, stored inline by the claiming CAS
     if (h < cap) {
       const ulonglong2 sl = reinterpret_cast<const ulonglong2*>(table)[h];
       if (sl.x != kEmptyKey) {
         cnt = (uint32_t)(sl.y >> 32) & kCntMask;
+        oflag = (uint32_t)(sl.y >> 32) & kOverflowBit;
         first = (uint32_t)sl.y;
       }
     }
@@ -294,10 +302,15 @@ __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_
       uint4 o;
       o.x = row(p0);
       o.y = row(p1);
-      o.z = cnt > 2 ? row(p2) : 0u;
-      o.w = cnt > 3 ? row(p3) : 0u;
-      *reinterpret_cast<uint4*>(grp) = o;
-      table[h].off = (uint32_t)(h * kInline);
+      if (cnt == 2 && o.y <= kPair2Row) {  // both rows in the slot (keeps the overflow flag)
+        reinterpret_cast<unsigned long long*>(table + h)[1] =
+            ((unsigned long long)(oflag | kPair2Bit | o.y) << 32) | o.x;
+      } else {
+        o.z = cnt > 2 ? row(p2) : 0u;
+        o.w = cnt > 3 ? row(p3) : 0u;
+        *reinterpret_cast<uint4*>(grp) = o;
+        table[h].off = (uint32_t)(h * kInline);
+      }
     }
     const uint32_t need = cnt > kInline ? cnt : 0u;  // big group: reserve its CSR range
     if (!__ballot_sync(0xFFFFFFFFu, need != 0)) continue;  // (almost every warp of slots)
@@ -783,9 +796,9 @@ __device__ __forceinline__ uint64_t warp_append_hits(unsigned lane, const uint32
   uint32_t nm = 0;
   uint64_t npr = 0;
 #pragma unroll
-  for (int j = 0; j < kWarpItems; ++j) {
+  for (int j = 0; j < kWarpItems; ++j) {  // cnt[j]: the slot's cnt word (kPair2Bit: an inline pair)
     nm += cnt[j] != 0;
-    npr += cnt[j];
+    npr += slot_members(cnt[j]);
   }
   // hits of the lanes before this one, and of the tile: one ballot per hit count
   const unsigned lt = (1u << lane) - 1u;
@@ -1112,14 +1125,15 @@ __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch s
       of[q] = 0;
       if (i < ne) {
         const uint64_t v = __ldcs(reinterpret_cast<const unsigned long long*>(sc.oc) + e0 + i);
-        c[q] = (uint32_t)(v >> 32);
+        c[q] = (uint32_t)(v >> 32);  // the slot's cnt word
         of[q] = (uint32_t)v;
         pr[q] = __ldcs(sc.prow + e0 + i);
-
       }
     }
 #pragma unroll
     for (int q = 0; q < kBatch; ++q) {
+      const uint32_t cw = c[q];
+      c[q] = slot_members(cw);
       uint64_t incl;
       if (__any_sync(0xFFFFFFFFu, c[q] >= (1u << 26))) {  // huge key groups: 64-bit scan
         incl = c[q];
@@ -1142,6 +1156,15 @@ __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch s
         if (g < cap) {
           st_hint(out_p + g, pr[q], pol_stream);
           st_hint(out_b + g, of[q] + rb, pol_stream);
+        }
+      } else if (cw & kPair2Bit) {  // an inline pair: both rows came with the slot
+        if (g < cap) {
+          st_hint(out_p + g, pr[q], pol_stream);
+          st_hint(out_b + g, of[q], pol_stream);
+        }
+        if (g + 1 < cap) {
+          st_hint(out_p + g + 1, pr[q], pol_stream);
+          st_hint(out_b + g + 1, cw & kPair2Row, pol_stream);
         }
       } else {
         // a key group: its rows are contiguous (CSR / side array); four

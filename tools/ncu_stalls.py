@@ -1,5 +1,5 @@
 """Stall-reason split, headline counters and the hottest SASS lines of one kernel in an ncu report.
-python tools/ncu_stalls.py report.ncu-rep [top_n]"""
+python tools/ncu_stalls.py report.ncu-rep [top_n] [kernel-name regex]"""
 import csv
 import io
 import subprocess
@@ -7,6 +7,7 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+kfilt = ["-k", f"regex:{sys.argv[3]}"] if len(sys.argv) > 3 else []
 
 
 def num(x):
@@ -16,7 +17,7 @@ def num(x):
         return 0.0
 
 
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = subprocess.run(["ncu", "-i", rep, *kfilt, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(raw)))
 d = dict(zip(r[0], r[2]))
 stalls = {k: num(v) for k, v in d.items() if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")}
@@ -29,7 +30,7 @@ for k in ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.s
     print(f"  {k} = {d.get(k)}")
 for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:10]:
     print(f"  stall {k.replace('smsp__pcsamp_warps_issue_stalled_', ''):22s} {100 * v / tot:5.1f}%")
-sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
+sass = subprocess.run(["ncu", "-i", rep, *kfilt, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                       text=True).stdout
 r = list(csv.reader(io.StringIO(sass)))
 h = r[1]
