@@ -922,6 +922,37 @@ constexpr int kPartProbeItems = GOLP_PART_PROBE_ITEMS;
 #define GOLP_PART_PROBE_SUB 8
 #endif
 constexpr int kPartProbeSub = GOLP_PART_PROBE_SUB;
+// Deferred second rounds: a key not resolved by its home pair is queued (per
+// warp, in shared memory) instead of holding its whole warp for another round
+// trip; a full queue is resolved by the warp with all 32 lanes busy. res_part
+// is indexed by entry, so the order in which entries resolve does not matter.
+#ifndef GOLP_PART_PROBE_QUEUE
+#define GOLP_PART_PROBE_QUEUE 1
+#endif
+struct PartProbeQueue {
+  uint64_t bits[32];
+  uint32_t h[32];
+  uint32_t i[32];  // entry index inside the span (< 2^32)
+};
+
+// Resolves this lane's queued key (lane < qn) to the end of its probe walk.
+__device__ __forceinline__ void part_queue_drain(const PartProbeQueue& q, unsigned lane, unsigned qn,
+                                                 const Slot* __restrict__ table, uint64_t mask,
+                                                 uint64_t* __restrict__ res_part, uint64_t pol_table) {
+  __syncwarp();
+  if (lane < qn) {
+    const uint64_t bits = q.bits[lane];
+    uint32_t h = q.h[lane], off = 0, cnt = 0;
+    for (;;) {
+      const int st = check_pair(ldg_pair(table + h, pol_table), bits, off, cnt, false);
+      if (st >= 0) break;
+      h = (h + 2) & (uint32_t)mask;
+    }
+    res_part[q.i[lane]] = ((uint64_t)cnt << 32) | off;
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_probe_part_kernel(const double* __restrict__ keys, uint64_t n,
                                                                         const Slot* __restrict__ table, uint64_t mask,
                                                                         uint64_t* __restrict__ res_part,
@@ -932,6 +963,13 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_prob
   const uint64_t sub = (uint64_t)kProbeThreads * kPartProbeItems;
   const uint64_t chunk = sub * kPartProbeSub;
   const uint64_t nchunks = (n + chunk - 1) / chunk;
+#if GOLP_PART_PROBE_QUEUE
+  static_assert(kPartProbeItems == 1, "the deferred queue takes one entry per lane and sub-tile");
+  __shared__ PartProbeQueue s_q[kProbeWarps];
+  const unsigned lane = lane_id();
+  PartProbeQueue& q = s_q[threadIdx.x >> 5];
+  unsigned qn = 0;  // queued entries of this warp (warp-uniform)
+#endif
   for (uint64_t c = sched.first(&s_t); c < nchunks; c = sched.next(c, &s_t)) {
     const uint64_t c0 = c * chunk + threadIdx.x;
     double kc[kPartProbeItems];
@@ -949,6 +987,36 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_prob
         const uint64_t i = base + sub + (uint64_t)j * kProbeThreads;
         kn[j] = (u + 1 < kPartProbeSub && i < n) ? ldg_stream_f64(keys + i, pol_stream) : 0.0;
       }
+#if GOLP_PART_PROBE_QUEUE
+      {
+        const uint64_t bits = canon_bits(kc[0]);
+        uint32_t h = home_slot32(bits, (uint32_t)mask), off = 0, cnt = 0;
+        const bool valid = base < n;
+        int st = 1;
+        if (valid) {
+          st = check_pair(ldg_pair(table + h, pol_table), bits, off, cnt, true);
+          if (st >= 0) res_part[base] = ((uint64_t)cnt << 32) | off;
+        }
+        unsigned need = __ballot_sync(0xFFFFFFFFu, st < 0);
+        while (need) {  // queue the unresolved lanes; resolve the queue whenever it fills
+          const unsigned room = 32u - qn;
+          const unsigned take = __popc(need) <= room ? need : need & ((1u << (__fns(need, 0, room + 1))) - 1u);
+          if ((take >> lane) & 1u) {
+            const unsigned pos = qn + __popc(take & ((1u << lane) - 1u));
+            q.bits[pos] = bits;
+            q.h[pos] = (h + 2) & (uint32_t)mask;
+            q.i[pos] = (uint32_t)base;
+          }
+          qn += __popc(take);
+          need &= ~take;
+          if (qn == 32u) {
+            part_queue_drain(q, lane, 32u, table, mask, res_part, pol_table);
+            qn = 0;
+          }
+        }
+        kc[0] = kn[0];
+      }
+#else
       uint64_t bits[kPartProbeItems];
       uint32_t h[kPartProbeItems], off[kPartProbeItems], cnt[kPartProbeItems];
       unsigned pending = 0;
@@ -981,8 +1049,12 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_prob
         if (i < n) res_part[i] = ((uint64_t)cnt[j] << 32) | off[j];
         kc[j] = kn[j];
       }
+#endif
     }
   }
+#if GOLP_PART_PROBE_QUEUE
+  if (qn) part_queue_drain(q, lane, qn, table, mask, res_part, pol_table);
+#endif
 }
 
 // Match stage of the radix-partitioned probe: block b owns partition tile b
