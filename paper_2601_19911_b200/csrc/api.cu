@@ -962,15 +962,35 @@ int resident_grid(K kernel, int threads, size_t smem) {
 
 // Groups the entries of [keys, keys+n) by table slice into g.part_keys, with
 // positions (build) or in-tile indices + (tile, slice) runs (probe). 3 launches.
+#ifndef GOLP_PART_CAP
+#define GOLP_PART_CAP 1  // probe side: fixed-capacity slices + overflow area instead of a count pass
+#endif
+// Fixed slice capacity for n probe entries over P slices: the expected share
+// + 1/32 + one tile, in whole partition tiles (the lookup kernel's chunks
+// never straddle two slices); 0 = exact layout (count pass + scan).
+uint64_t probe_slice_capacity(uint64_t n, uint32_t P) {
+  if (!GOLP_PART_CAP || !env_u64("GOLP_PART_CAP", 1) || P < 2) return 0;
+  const uint64_t share = (n + P - 1) / P;
+  return (share + share / 32 + 2 * kPartTile) / kPartTile * kPartTile;
+}
+
+// Entries the partitioned probe buffers hold for n probes (slices + overflow area).
+uint64_t probe_part_entries(uint64_t n, uint32_t P) {
+  const uint64_t capu = probe_slice_capacity(n, P);
+  return capu ? (uint64_t)P * capu + n : n;
+}
+
 int partition_entries(const double* keys, uint64_t n, bool probe_side, cudaStream_t s) {
   Ctx& g = cur();
   const uint32_t P = g.jparts;
   const uint64_t ntiles = (n + kPartTile - 1) / kPartTile;
-  CK(g.part_keys.ensure(std::max<uint64_t>(n, 1) * 8));
-  CK(g.part_pos.ensure(std::max<uint64_t>(n, 1) * (probe_side ? 2 : 4)));
+  const uint64_t capu = probe_side ? probe_slice_capacity(n, P) : 0;
+  const uint64_t nall = probe_side ? probe_part_entries(n, P) : n;
+  CK(g.part_keys.ensure(std::max<uint64_t>(nall, 1) * 8));
+  CK(g.part_pos.ensure(std::max<uint64_t>(nall, 1) * (probe_side ? 2 : 4)));
   CK(g.part_cnt.ensure(P * 8));
-  CK(g.part_cur.ensure(P * 8));
-  PartOut o{g.part_keys.as<double>(), nullptr, nullptr, nullptr, nullptr};
+  CK(g.part_cur.ensure((P + 1) * 8));
+  PartOut o{g.part_keys.as<double>(), nullptr, nullptr, nullptr, nullptr, 0, nullptr};
   if (probe_side) {
     CK(g.run_base.ensure(std::max<uint64_t>(ntiles * P, 1) * 4));
     CK(g.run_len.ensure(std::max<uint64_t>(ntiles * P, 1) * 2));
@@ -982,17 +1002,24 @@ int partition_entries(const double* keys, uint64_t n, bool probe_side, cudaStrea
   }
   unsigned long long* cnt = g.part_cnt.as<unsigned long long>();
   unsigned long long* cursors = g.part_cur.as<unsigned long long>();
-  CK(cudaMemsetAsync(cnt, 0, P * 8, s));
-  part_count_kernel<<<g.sms * 4, kPartThreads, 0, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cnt);
-  CKL();
-  part_scan_kernel<<<1, 1024, 0, s>>>(cnt, cursors, P);
-  CKL();
+  if (capu) {  // slice cursors count from each slice's fixed base; cursors[P] = overflow area
+    CK(cudaMemsetAsync(cursors, 0, (P + 1) * 8, s));
+    o.capu = capu;
+    o.ovf = cursors + P;
+  } else {
+    CK(cudaMemsetAsync(cnt, 0, P * 8, s));
+    part_count_kernel<<<g.sms * 4, kPartThreads, 0, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cnt);
+    CKL();
+    part_scan_kernel<<<1, 1024, 0, s>>>(cnt, cursors, P);
+    CKL();
+    g_launches += 2;
+  }
   RET(smem_attr(part_scatter_kernel, kPartScatterSmem));
   const int gsmax = resident_grid(part_scatter_kernel, kPartThreads, kPartScatterSmem);
   const int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)gsmax));
   part_scatter_kernel<<<gs, kPartThreads, kPartScatterSmem, s>>>(keys, n, (uint32_t)g.jmask, g.jslice_bits, P, cursors, o);
   CKL();
-  g_launches += 3;
+  g_launches += 1;
   return GOLP_OK;
 }
 
@@ -1001,16 +1028,19 @@ int partition_entries(const double* keys, uint64_t n, bool probe_side, cudaStrea
 int probe_partitioned(const double* pkeys, uint64_t n, cudaStream_t s) {
   Ctx& g = cur();
   RET(partition_entries(pkeys, n, true, s));
-  CK(g.res_part.ensure(n * 8));
+  const uint64_t nall = probe_part_entries(n, g.jparts);
+  CK(g.res_part.ensure(nall * 8));
   const int grid = resident_grid(join_probe_part_kernel, kProbeThreads, 0);
   const int policy = (int)env_u64("GOLP_JOIN_PART_POLICY", 0);
   const uint64_t items = (uint64_t)kProbeThreads * kPartProbeItems;
-  const int gp = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + items - 1) / items, (uint64_t)grid));
+  const int gp = (int)std::max<uint64_t>(1, std::min<uint64_t>((nall + items - 1) / items, (uint64_t)grid));
   CK(g.work_ctr.ensure(8));
   CK(cudaMemsetAsync(g.work_ctr.p, 0, 8, s));
-  join_probe_part_kernel<<<gp, kProbeThreads, 0, s>>>(g.part_keys.as<double>(), n, g.table.as<Slot>(), g.jmask,
+  const unsigned long long* cursors = g.part_cur.as<unsigned long long>();
+  const PartExtent ext{probe_slice_capacity(n, g.jparts), g.jparts, cursors, cursors + g.jparts};
+  join_probe_part_kernel<<<gp, kProbeThreads, 0, s>>>(g.part_keys.as<double>(), nall, g.table.as<Slot>(), g.jmask,
                                                       g.res_part.as<uint64_t>(), policy,
-                                                      TileSched{g.work_ctr.as<unsigned long long>()});
+                                                      TileSched{g.work_ctr.as<unsigned long long>()}, ext);
   CKL();
   ++g_launches;
   return GOLP_OK;

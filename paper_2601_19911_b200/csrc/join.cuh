@@ -623,6 +623,12 @@ struct PartOut {
   uint16_t* idx;       // probe side: the entry's index inside its tile (or null)
   uint32_t* run_base;  // probe side: [tile * nparts + p] = offset of the tile's run of slice p
   uint16_t* run_len;   //             and its length
+  // Fixed-capacity layout (capu > 0, probe side): slice p owns [p * capu, (p+1) * capu)
+  // and cursors[p] counts its entries (no count pass); a run that does not fit
+  // goes to the overflow area at nparts * capu (cursor *ovf). Runs are located
+  // through run_base either way, so only locality suffers for skewed slices.
+  uint64_t capu;
+  unsigned long long* ovf;
 };
 
 // Exclusive scan of s_cnt[0..nparts) into s_start (nparts <= 2 * blockDim.x).
@@ -715,7 +721,11 @@ __global__ void __launch_bounds__(kPartThreads, GOLP_PART_MINB) part_scatter_ker
     block_scan_parts(s_cnt, s_start, nparts, s_w);
     for (uint32_t p = threadIdx.x; p < nparts; p += blockDim.x) {
       const unsigned c = s_cnt[p];
-      const unsigned long long b = c ? atomicAdd(&cursors[p], (unsigned long long)c) : 0ull;
+      unsigned long long b = c ? atomicAdd(&cursors[p], (unsigned long long)c) : 0ull;
+      if (out.capu && c) {
+        if (b + c <= out.capu) b += p * out.capu;
+        else b = (uint64_t)nparts * out.capu + atomicAdd(out.ovf, (unsigned long long)c);
+      }
       s_base[p] = b;
       if (out.run_base) {
         out.run_base[t * nparts + p] = (uint32_t)b;
@@ -953,16 +963,36 @@ __device__ __forceinline__ void part_queue_drain(const PartProbeQueue& q, unsign
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_probe_part_kernel(const double* __restrict__ keys, uint64_t n,
+// Fixed-capacity partitions (PartOut::capu): the valid part of each chunk.
+struct PartExtent {
+  uint64_t capu;                         // 0: the entries are dense in [0, n)
+  uint32_t nparts;
+  const unsigned long long* used;        // per slice: entries routed to it (may exceed capu)
+  const unsigned long long* ovf;         // entries in the overflow area
+  // end of the valid entries of the slice (or overflow area) holding position c0
+  __device__ __forceinline__ uint64_t end_of(uint64_t c0, uint64_t n) const {
+    if (!capu) return n;
+    const uint64_t p = c0 / capu;
+    if (p < nparts) {
+      const unsigned long long u = __ldcg(used + p);
+      return p * capu + (u < capu ? u : capu);
+    }
+    return (uint64_t)nparts * capu + __ldcg(ovf);
+  }
+};
+
+__global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_probe_part_kernel(const double* __restrict__ keys, uint64_t n_all,
                                                                         const Slot* __restrict__ table, uint64_t mask,
                                                                         uint64_t* __restrict__ res_part,
-                                                                        int table_policy, TileSched sched) {
+                                                                        int table_policy, TileSched sched,
+                                                                        PartExtent ext) {
+  __shared__ uint64_t s_end;
   __shared__ unsigned long long s_t;
   const uint64_t pol_table = table_policy ? policy_evict_normal() : policy_evict_last();
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t sub = (uint64_t)kProbeThreads * kPartProbeItems;
   const uint64_t chunk = sub * kPartProbeSub;
-  const uint64_t nchunks = (n + chunk - 1) / chunk;
+  const uint64_t nchunks = (n_all + chunk - 1) / chunk;
 #if GOLP_PART_PROBE_QUEUE
   static_assert(kPartProbeItems == 1, "the deferred queue takes one entry per lane and sub-tile");
   __shared__ PartProbeQueue s_q[kProbeWarps];
@@ -971,6 +1001,10 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_prob
   unsigned qn = 0;  // queued entries of this warp (warp-uniform)
 #endif
   for (uint64_t c = sched.first(&s_t); c < nchunks; c = sched.next(c, &s_t)) {
+    // valid entries end at n (chunks never straddle fixed-capacity slices)
+    if (threadIdx.x == 0) s_end = ext.end_of(c * chunk, n_all);
+    __syncthreads();
+    const uint64_t n = s_end;
     const uint64_t c0 = c * chunk + threadIdx.x;
     double kc[kPartProbeItems];
 #pragma unroll

@@ -173,6 +173,27 @@ def test_partitioned_join_multi_span(b200, monkeypatch, span):
     assert np.array_equal(res.payload.build_rows, eb)
 
 
+@pytest.mark.parametrize("hot", [0.3, 0.97, 1.0])
+def test_partitioned_probe_hot_key_overflows_slice(b200, monkeypatch, hot):
+    """Probe sides whose slices are far from balanced (one key is 30% .. 100%
+    of the probes): the fixed-capacity slice of the hot key overflows and its
+    runs go to the overflow area; pairs and order must not change."""
+    monkeypatch.setenv("GOLP_JOIN_SLICE_BYTES", "65536")
+    monkeypatch.setenv("GOLP_JOIN_PART_PROBE", "1")
+    rng = np.random.default_rng(int(hot * 100))
+    nb, np_ = 60_000, 400_000
+    bk = rng.integers(0, 120_000, size=nb).astype(np.float64)
+    nhot = int(np_ * hot)
+    pk = np.concatenate([np.full(nhot, bk[7]), rng.integers(0, 120_000, size=np_ - nhot).astype(np.float64)])
+    pk = rng.permutation(pk)
+    br = rng.permutation(nb).astype(np.uint32)
+    pr = np.arange(np_, dtype=np.uint32)
+    res = b200.probe(KeyVector(bk, br), KeyVector(pk, pr))
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert res.payload.match_count == len(ep)
+    assert np.array_equal(res.payload.probe_rows, ep) and np.array_equal(res.payload.build_rows, eb)
+
+
 def test_partitioned_join_natural_scale(cuda):
     """A table above the partitioning threshold with default settings (1 GiB
     table, 64 slices, probe side partitioned) against the oracle."""
