@@ -154,13 +154,16 @@ def test_partitioned_join_resident_subchunks(cuda, monkeypatch):
     assert np.array_equal(ob.cpu().numpy().view(np.uint32), eb)
 
 
+@pytest.mark.parametrize("layout", ["slice", "exact"])
 @pytest.mark.parametrize("span", ["4096", "12288"])
-def test_partitioned_join_multi_span(b200, monkeypatch, span):
+def test_partitioned_join_multi_span(b200, monkeypatch, span, layout):
     """Probe sides longer than a span are partitioned span by span; pair offsets
-    chain across spans and sub-chunks."""
+    chain across spans and sub-chunks (each partition layout)."""
     monkeypatch.setenv("GOLP_JOIN_SLICE_BYTES", "4096")
     monkeypatch.setenv("GOLP_JOIN_PART_PROBE", "1")
     monkeypatch.setenv("GOLP_JOIN_SPAN", span)
+    if layout == "exact":
+        monkeypatch.setenv("GOLP_PART_CAP", "0")
     rng = np.random.default_rng(int(span))
     nb, np_ = 40_000, 90_001
     bk = rng.integers(0, 60_000, size=nb).astype(np.float64)
@@ -173,7 +176,7 @@ def test_partitioned_join_multi_span(b200, monkeypatch, span):
     assert np.array_equal(res.payload.build_rows, eb)
 
 
-@pytest.mark.parametrize("hot", [0.3, 0.97, 1.0])
+@pytest.mark.parametrize("hot", [0.0, 0.3, 0.97, 1.0])
 def test_partitioned_probe_hot_key_overflows_slice(b200, monkeypatch, hot):
     """Probe sides whose slices are far from balanced (one key is 30% .. 100%
     of the probes): the fixed-capacity slice of the hot key overflows and its
