@@ -112,7 +112,7 @@ struct Ctx {
   cudaEvent_t ev_rows = nullptr;  // a copied row column of a chunked upload has landed
 
   DevBuf ctl, cand_hi, cand_lo, w_hi, w_lo, out_rows, out_hi, samples;
-  DevBuf table, rows_arr, ovf, big_list, jcount, wcount, partial, totals, totals2;
+  DevBuf table, rows_arr, ovf, big_list, grp_bits, jcount, wcount, partial, totals, totals2;
   DevBuf sc_prow, sc_oc;
   DevBuf part_keys, part_pos, part_cnt, part_cur, run_base, run_len, res_part, work_ctr;
   DevBuf pairs_p, pairs_b;
@@ -1053,6 +1053,9 @@ int probe_partitioned(const double* pkeys, uint64_t n, cudaStream_t s) {
 // position (the emit adds rows[0]): the finalize neither gathers nor stores them.
 constexpr uint64_t kDenseCheckMin = 256u << 10;
 
+#ifndef GOLP_GROUP_BITS_MIN_CAP
+#define GOLP_GROUP_BITS_MIN_CAP (1ull << 20)
+#endif
 int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cudaStream_t s, int rows_dense = 0) {
   Ctx& g = cur();
   uint64_t cap = 1024;
@@ -1092,8 +1095,14 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   ga.ovf_pos = ga.ovf_rank + nbb;
   ga.counters = g.jcount.as<unsigned long long>();
   ga.big_list = g.big_list.as<uint32_t>();
+  // key groups flagged in a slot bitmap: a dense build's finalize visits only them
+  ga.grp_bits = nullptr;
+  if (cap >= env_u64("GOLP_GROUP_BITS_MIN_CAP", GOLP_GROUP_BITS_MIN_CAP)) {
+    CK(g.grp_bits.ensure((cap + 31) / 32 * 4));
+    ga.grp_bits = g.grp_bits.as<uint32_t>();
+  }
   prof_record(4, s);
-  join_init_table_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap);
+  join_init_table_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, ga.grp_bits);
   CKL();
   ++g_launches;
   CK(cudaMemsetAsync(g.jcount.p, 0, 32, s));
@@ -1363,7 +1372,7 @@ void release_context(Ctx& g) {
   for (cudaStream_t st : {g.s_main, g.s_h2d, g.s_d2h}) cudaStreamSynchronize(st);
   g.pool.stop();
   DevBuf* bufs[] = {&g.ctl, &g.cand_hi, &g.cand_lo, &g.w_hi, &g.w_lo, &g.out_rows, &g.out_hi, &g.samples,
-                    &g.table, &g.rows_arr, &g.ovf, &g.big_list, &g.jcount,
+                    &g.table, &g.rows_arr, &g.ovf, &g.big_list, &g.grp_bits, &g.jcount,
                     &g.wcount, &g.partial, &g.totals, &g.totals2, &g.sc_prow, &g.sc_oc, &g.part_keys, &g.part_pos, &g.part_cnt, &g.part_cur, &g.run_base, &g.run_len, &g.res_part, &g.work_ctr, &g.pairs_p, &g.pairs_b, &g.srt_hist, &g.srt_k0, &g.srt_k1, &g.srt_r0, &g.srt_r1, &g.srt_status, &g.srt_base, &g.in_keys, &g.in_rows,
                     &g.in_bkeys, &g.in_brows, &g.in_payload, &g.rows_flag, &g.row_base};
   for (DevBuf* b : bufs) b->release();

@@ -89,10 +89,11 @@ constexpr uint32_t kPair2Row = kPair2Bit - 1u;
 __host__ __device__ __forceinline__ uint32_t slot_members(uint32_t cw) { return (cw & kPair2Bit) ? 2u : cw; }
 constexpr uint32_t kGroupTile = 16384;  // big groups up to this size sorted in shared memory (64 KB)
 
-__global__ void join_init_table_kernel(Slot* __restrict__ table, uint64_t cap) {
+__global__ void join_init_table_kernel(Slot* __restrict__ table, uint64_t cap, uint32_t* __restrict__ grp_bits) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += stride) {
     reinterpret_cast<ulonglong2*>(table)[i] = make_ulonglong2(kEmptyKey, 0ull);
+    if (grp_bits && (i & 31) == 0) grp_bits[i >> 5] = 0u;
   }
 }
 
@@ -116,6 +117,7 @@ struct GroupArrays {
   uint32_t* ovf_pos;
   unsigned long long* counters;  // [0] overflow count, [1] CSR cursor, [2] big groups, [3] of them > kThreadGroup
   uint32_t* big_list;  // big groups, then (appended) the ones above kThreadGroup
+  uint32_t* grp_bits;  // or null: one bit per slot, set when the slot's key gets a second member
 };
 
 // Tile schedule of kernels that walk slice-partitioned entries: with a counter,
@@ -212,6 +214,9 @@ __global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double
 #pragma unroll
     for (int j = 0; j < kBuildItems; ++j)
       if (dup & (1u << j)) r[j] = atomicAdd(&table[h[j]].cnt, 1u) & kCntMask;
+#pragma unroll
+    for (int j = 0; j < kBuildItems; ++j)  // a key's second member marks its slot for the finalize
+      if (ga.grp_bits && ((dup >> j) & 1u) && r[j] == 1) atomicOr(&ga.grp_bits[h[j] >> 5], 1u << (h[j] & 31));
     if constexpr (!kWide) {
 #pragma unroll
       for (int j = 0; j < kBuildItems; ++j)
@@ -275,14 +280,29 @@ __device__ __forceinline__ void cswap_u32(uint32_t& a, uint32_t& b) {
 // their recorded positions and turn them into rows, big groups reserve a CSR range.
 // Dense row column: singletons keep their build POSITION in slot.off (the emit
 // adds the column's first row id, *row_base): no gather and no store for them.
+// Dense row column with ga.grp_bits: singletons need nothing, so lane l of a
+// warp takes the 8 slots of bitmap byte wb + l and visits its flagged key
+// groups one per step, instead of every slot of the table.
 __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_t cap, BuildRows br,
                                                             GroupArrays ga, uint64_t csr_base, uint32_t* row_base) {
   const unsigned lane = lane_id();
   const RowMap row(br);
   if (blockIdx.x == 0 && threadIdx.x == 0) *row_base = row.dense ? row.base : 0u;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t wb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; wb < cap; wb += stride) {
-    const uint64_t h = wb + lane;
+  const bool use_bits = row.dense && ga.grp_bits;
+  const uint64_t nvisit = use_bits ? (cap + 7) / 8 : cap;
+  const uint8_t* gbytes = reinterpret_cast<const uint8_t*>(ga.grp_bits);
+  for (uint64_t wb = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; wb < nvisit; wb += stride) {
+    uint32_t bits = use_bits && wb + lane < nvisit ? gbytes[wb + lane] : 0u;
+    for (;;) {
+    uint64_t h;
+    if (use_bits) {
+      if (!__any_sync(0xFFFFFFFFu, bits != 0)) break;
+      h = bits ? (wb + lane) * 8 + (uint32_t)__ffs(bits) - 1 : cap;
+      bits &= bits - 1;
+    } else {
+      h = wb + lane;
+    }
     uint32_t cnt = 0, first = 0, oflag = 0;  // first: rank-0 position, stored inline by the claiming CAS
     if (h < cap) {
       const ulonglong2 sl = reinterpret_cast<const ulonglong2*>(table)[h];
@@ -313,7 +333,10 @@ __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_
       }
     }
     const uint32_t need = cnt > kInline ? cnt : 0u;  // big group: reserve its CSR range
-    if (!__ballot_sync(0xFFFFFFFFu, need != 0)) continue;  // (almost every warp of slots)
+    if (!__ballot_sync(0xFFFFFFFFu, need != 0)) {  // (almost every warp of slots)
+      if (use_bits) continue;
+      break;
+    }
     unsigned long long incl = need;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -332,6 +355,8 @@ __global__ void __launch_bounds__(256) join_finalize_kernel(Slot* table, uint64_
       ga.rows[off + 2] = v.z;
       ga.rows[off + 3] = v.w;
       ga.big_list[atomicAdd(&ga.counters[2], 1ull)] = (uint32_t)h;
+    }
+    if (!use_bits) break;
     }
   }
 }

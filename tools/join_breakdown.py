@@ -24,12 +24,15 @@ op = torch.empty(cap, dtype=torch.int32, device="cuda")
 ob = torch.empty(cap, dtype=torch.int32, device="cuda")
 resident.set_profiling(True)
 bt, pt = [], []
-for i in range(reps):
+for i in range(reps + 1):  # the first call (allocations) is dropped
     resident.join_build(bk, br)
     m = resident.join_probe(pk, pr, op, ob)
     kt = _native.kernel_times()
-    bt.append(kt["join_build_ms"])
-    pt.append(kt["join_probe_ms"])
+    if i:
+        bt.append(kt["join_build_ms"])
+        pt.append(kt["join_probe_ms"])
 resident.set_profiling(False)
 print(f"nb={nb:,} np={np_:,} dom={dom:,} slices={kt['join_slices']} cap={kt['join_capacity']:,} M={m:,}: "
       f"build {statistics.median(bt):.3f} ms probe {statistics.median(pt):.3f} ms")
+if "-v" in sys.argv:
+    print("  probe ms per rep:", " ".join(f"{x:.3f}" for x in pt))
