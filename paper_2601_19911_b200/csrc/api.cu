@@ -1082,11 +1082,7 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   unsigned* dflag = g.rows_flag.as<unsigned>();
   const bool check = !rows_dense && nb >= kDenseCheckMin;
   CK(cudaMemsetAsync(dflag, (rows_dense || check) ? 1 : 0, 4, s));  // byte value 1 -> nonzero word
-  if (check) {
-    dense_rows_check_kernel<<<g.sms * 4, 256, 0, s>>>(brows, nb, dflag);
-    CKL();
-    ++g_launches;
-  }
+  // (the check itself runs inside join_init_table_kernel)
   const BuildRows br{brows, dflag};
   GroupArrays ga;
   ga.rows = g.rows_arr.as<uint32_t>();
@@ -1102,7 +1098,8 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
     ga.grp_bits = g.grp_bits.as<uint32_t>();
   }
   prof_record(4, s);
-  join_init_table_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, ga.grp_bits);
+  join_init_table_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, ga.grp_bits, brows, check ? nb : 0,
+                                                                dflag);
   CKL();
   ++g_launches;
   CK(cudaMemsetAsync(g.jcount.p, 0, 32, s));

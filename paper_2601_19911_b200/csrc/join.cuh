@@ -89,12 +89,31 @@ constexpr uint32_t kPair2Row = kPair2Bit - 1u;
 __host__ __device__ __forceinline__ uint32_t slot_members(uint32_t cw) { return (cw & kPair2Bit) ? 2u : cw; }
 constexpr uint32_t kGroupTile = 16384;  // big groups up to this size sorted in shared memory (64 KB)
 
-__global__ void join_init_table_kernel(Slot* __restrict__ table, uint64_t cap, uint32_t* __restrict__ grp_bits) {
+// Empties the table (and the group bitmap); with check_n > 0 it also runs the
+// build row column's density check (see dense_rows_check_kernel) in the same launch.
+__device__ __forceinline__ bool rows_not_dense(const uint32_t* __restrict__ rows, uint64_t n) {
+  const uint32_t b0 = rows[0];
+  bool bad = false;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t n4 = ((reinterpret_cast<uintptr_t>(rows) & 15) == 0) ? n / 4 : 0;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(rows) + q);
+    const uint32_t e = b0 + (uint32_t)(4 * q);
+    bad |= (v.x != e) | (v.y != e + 1u) | (v.z != e + 2u) | (v.w != e + 3u);
+  }
+  for (uint64_t i = 4 * n4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    bad |= rows[i] != b0 + (uint32_t)i;
+  return bad;
+}
+
+__global__ void join_init_table_kernel(Slot* __restrict__ table, uint64_t cap, uint32_t* __restrict__ grp_bits,
+                                       const uint32_t* __restrict__ rows, uint64_t check_n, unsigned* flag) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += stride) {
     reinterpret_cast<ulonglong2*>(table)[i] = make_ulonglong2(kEmptyKey, 0ull);
     if (grp_bits && (i & 31) == 0) grp_bits[i >> 5] = 0u;
   }
+  if (check_n && __syncthreads_or(rows_not_dense(rows, check_n)) && threadIdx.x == 0) *flag = 0u;
 }
 
 // Build kernels process tiles of kBuildThreads*kBuildItems consecutive entries;
@@ -254,21 +273,6 @@ struct RowMap {
   __device__ __forceinline__ uint32_t operator()(uint32_t p) const { return dense ? base + p : __ldg(rows + p); }
 };
 
-// *flag (preset to 1) is cleared unless rows[i] == rows[0] + i for every i < n.
-__global__ void dense_rows_check_kernel(const uint32_t* __restrict__ rows, uint64_t n, unsigned* flag) {
-  const uint32_t b0 = rows[0];
-  bool bad = false;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t n4 = ((reinterpret_cast<uintptr_t>(rows) & 15) == 0) ? n / 4 : 0;
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {
-    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(rows) + q);
-    const uint32_t e = b0 + (uint32_t)(4 * q);
-    bad |= (v.x != e) | (v.y != e + 1u) | (v.z != e + 2u) | (v.w != e + 3u);
-  }
-  for (uint64_t i = 4 * n4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    bad |= rows[i] != b0 + (uint32_t)i;
-  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 0u;
-}
 
 __device__ __forceinline__ void cswap_u32(uint32_t& a, uint32_t& b) {
   const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
