@@ -1099,10 +1099,9 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   }
   prof_record(4, s);
   join_init_table_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, ga.grp_bits, brows, check ? nb : 0,
-                                                                dflag);
+                                                                dflag, ga.counters);
   CKL();
   ++g_launches;
-  CK(cudaMemsetAsync(g.jcount.p, 0, 32, s));
   if (nb == 0) {
     prof_record(5, s);
     return GOLP_OK;
@@ -1155,8 +1154,9 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
 int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
                  uint64_t cap, const unsigned long long* base_in, unsigned long long* total_out, cudaStream_t s) {
   Ctx& g = cur();
-  if (np == 0 || g.jnb == 0) {
-    CK(cudaMemcpyAsync(total_out, base_in, 8, cudaMemcpyDeviceToDevice, s));
+  if (np == 0 || g.jnb == 0) {  // base_in null: no pairs before this probe
+    if (base_in) CK(cudaMemcpyAsync(total_out, base_in, 8, cudaMemcpyDeviceToDevice, s));
+    else CK(cudaMemsetAsync(total_out, 0, 8, s));
     return GOLP_OK;
   }
   // Partition the probe side (in spans of kSpan probes) when a span reuses each
@@ -1248,9 +1248,8 @@ int join_probe_impl(const double* pkeys, const uint32_t* prows, uint64_t np, uin
   Ctx& g = cur();
   CK(g.totals.ensure(16));
   unsigned long long* totals = g.totals.as<unsigned long long>();
-  CK(cudaMemsetAsync(totals, 0, 16, s));
   prof_record(6, s);
-  RET(launch_probe(pkeys, prows, np, out_p, out_b, cap, totals, totals + 1, s));
+  RET(launch_probe(pkeys, prows, np, out_p, out_b, cap, nullptr, totals + 1, s));
   prof_record(7, s);
   RET(read_probe_total(totals + 1, out_m, s));
   if (g.prof) g.kt.join_probe_ms = prof_ms(6, 7);
@@ -1651,11 +1650,8 @@ int golp_join_probe_device_async(const double* d_probe_keys, const uint32_t* d_p
   if (!d_out_matches) return invalid("null d_out_matches");
   RET(check_device_ptr(d_probe_keys));
   cudaStream_t s = as_stream(stream);
-  CK(g.totals.ensure(16));
-  unsigned long long* totals = g.totals.as<unsigned long long>();
-  CK(cudaMemsetAsync(totals, 0, 8, s));
   prof_record(6, s);
-  RET(launch_probe(d_probe_keys, d_probe_rows, np, d_out_probe_rows, d_out_build_rows, cap, totals,
+  RET(launch_probe(d_probe_keys, d_probe_rows, np, d_out_probe_rows, d_out_build_rows, cap, nullptr,
                    reinterpret_cast<unsigned long long*>(d_out_matches), s));
   prof_record(7, s);
   g.probe_timed = g.prof;  // resolved lazily by golp_last_kernel_times

@@ -107,8 +107,10 @@ __device__ __forceinline__ bool rows_not_dense(const uint32_t* __restrict__ rows
 }
 
 __global__ void join_init_table_kernel(Slot* __restrict__ table, uint64_t cap, uint32_t* __restrict__ grp_bits,
-                                       const uint32_t* __restrict__ rows, uint64_t check_n, unsigned* flag) {
+                                       const uint32_t* __restrict__ rows, uint64_t check_n, unsigned* flag,
+                                       unsigned long long* __restrict__ counters) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  if (blockIdx.x == 0 && threadIdx.x < 4) counters[threadIdx.x] = 0ull;  // GroupArrays::counters
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += stride) {
     reinterpret_cast<ulonglong2*>(table)[i] = make_ulonglong2(kEmptyKey, 0ull);
     if (grp_bits && (i & 31) == 0) grp_bits[i >> 5] = 0u;
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(unsigned lo
                                                                      const unsigned long long* base_in,
                                                                      unsigned long long* total_out) {
   __shared__ unsigned long long s_w[33];
-  unsigned long long carry = *base_in;
+  unsigned long long carry = base_in ? *base_in : 0ull;  // null: the probe's first pairs
   for (uint32_t b0 = 0; b0 < nparts; b0 += blockDim.x) {
     const uint32_t i = b0 + threadIdx.x;
     const unsigned long long v = i < nparts ? partial[i] : 0ull;
@@ -1236,7 +1238,7 @@ __global__ void __launch_bounds__(kProbeThreads) join_emit_kernel(MatchScratch s
   if constexpr (kScanned) {
     run = bpart[blockIdx.x];
   } else {
-    run = *base_in;
+    run = base_in ? *base_in : 0ull;
     for (unsigned w = 0; w < kProbeWarps; ++w) run += s_red[w];
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total_out = run + __ldcg(bpart + blockIdx.x);
   }
