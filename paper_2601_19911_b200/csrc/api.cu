@@ -116,7 +116,7 @@ struct Ctx {
   DevBuf sc_prow, sc_oc;
   DevBuf part_keys, part_pos, part_cnt, part_cur, run_base, run_len, res_part, work_ctr;
   DevBuf pairs_p, pairs_b;
-  DevBuf rows_flag;  // build row column is a dense run (join_build_impl)
+  DevBuf rows_flag;  // two words: the build row column is NOT a dense run (alternate builds, join_build_impl)
   DevBuf row_base;   // what the emit adds to a singleton's slot.off (rows[0] for a dense column, else 0)
   DevBuf srt_hist, srt_k0, srt_k1, srt_r0, srt_r1, srt_status, srt_base;
   DevBuf in_keys, in_rows, in_bkeys, in_brows, in_payload;
@@ -130,6 +130,7 @@ struct Ctx {
   uint64_t moved_h2d = 0, moved_d2h = 0;
   bool dense_rows = true;  // GOLP_DENSE_ROWS=0 ships every row-id column
   bool rows_hint = false;
+  unsigned build_parity = 0;  // which rows_flag word the next build uses
   int prof_last = -1, probe_start_ev = 6;  // prof_record: last event recorded, probe start event
   cudaStream_t prof_last_stream = nullptr;
   uint64_t prof_last_launches = 0;  // golp_hint_dense_rows: the next call's row columns are positions
@@ -1091,10 +1092,15 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   g.kt.join_capacity = cap;
   g.kt.join_slices = g.jparts;
   Slot* table = g.table.as<Slot>();
-  CK(g.rows_flag.ensure(4));
-  unsigned* dflag = g.rows_flag.as<unsigned>();
+  // two "not dense" words, used by alternate builds (see join_init_table_kernel)
+  if (!g.rows_flag.p) {
+    CK(g.rows_flag.ensure(8));
+    CK(cudaMemsetAsync(g.rows_flag.p, 0, 8, s));
+  }
+  unsigned* dflag = g.rows_flag.as<unsigned>() + g.build_parity;
+  unsigned* dflag_next = g.rows_flag.as<unsigned>() + (g.build_parity ^ 1);
+  g.build_parity ^= 1;
   const bool check = !rows_dense && nb >= kDenseCheckMin;
-  CK(cudaMemsetAsync(dflag, (rows_dense || check) ? 1 : 0, 4, s));  // byte value 1 -> nonzero word
   // (the check itself runs inside join_init_table_kernel)
   const BuildRows br{brows, dflag};
   GroupArrays ga;
@@ -1111,8 +1117,9 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
     ga.grp_bits = g.grp_bits.as<uint32_t>();
   }
   prof_record(4, s);
-  join_init_table_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, ga.grp_bits, brows, check ? nb : 0,
-                                                                dflag, ga.counters);
+  join_init_table_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, ga.grp_bits, brows, nb,
+                                                                check ? 0 : (rows_dense ? 1 : 2), dflag, dflag_next,
+                                                                ga.counters);
   CKL();
   ++g_launches;
   if (nb == 0) {

@@ -89,8 +89,11 @@ constexpr uint32_t kPair2Row = kPair2Bit - 1u;
 __host__ __device__ __forceinline__ uint32_t slot_members(uint32_t cw) { return (cw & kPair2Bit) ? 2u : cw; }
 constexpr uint32_t kGroupTile = 16384;  // big groups up to this size sorted in shared memory (64 KB)
 
-// Empties the table (and the group bitmap); with check_n > 0 it also runs the
-// build row column's density check (see dense_rows_check_kernel) in the same launch.
+// Empties the table (and the group bitmap) and settles the build row column's
+// density flag *nd (0 = dense): mode 0 checks the column (*nd is 0 on entry and
+// is set on a mismatch), 1 = declared dense, 2 = not dense (unchecked). The
+// flag word of the next build, *nd_next, is cleared here, so no separate
+// memset is needed before its check.
 __device__ __forceinline__ bool rows_not_dense(const uint32_t* __restrict__ rows, uint64_t n) {
   const uint32_t b0 = rows[0];
   bool bad = false;
@@ -107,15 +110,19 @@ __device__ __forceinline__ bool rows_not_dense(const uint32_t* __restrict__ rows
 }
 
 __global__ void join_init_table_kernel(Slot* __restrict__ table, uint64_t cap, uint32_t* __restrict__ grp_bits,
-                                       const uint32_t* __restrict__ rows, uint64_t check_n, unsigned* flag,
-                                       unsigned long long* __restrict__ counters) {
+                                       const uint32_t* __restrict__ rows, uint64_t n, int mode, unsigned* nd,
+                                       unsigned* nd_next, unsigned long long* __restrict__ counters) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   if (blockIdx.x == 0 && threadIdx.x < 4) counters[threadIdx.x] = 0ull;  // GroupArrays::counters
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *nd_next = 0u;
+    if (mode != 0) *nd = mode == 2 ? 1u : 0u;
+  }
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += stride) {
     reinterpret_cast<ulonglong2*>(table)[i] = make_ulonglong2(kEmptyKey, 0ull);
     if (grp_bits && (i & 31) == 0) grp_bits[i >> 5] = 0u;
   }
-  if (check_n && __syncthreads_or(rows_not_dense(rows, check_n)) && threadIdx.x == 0) *flag = 0u;
+  if (mode == 0 && __syncthreads_or(rows_not_dense(rows, n)) && threadIdx.x == 0) *nd = 1u;
 }
 
 // Build kernels process tiles of kBuildThreads*kBuildItems consecutive entries;
@@ -264,14 +271,14 @@ __global__ void __launch_bounds__(kBuildThreads) join_insert_kernel(const double
 // the column outgrows L2 -- is skipped.
 struct BuildRows {
   const uint32_t* rows;
-  const unsigned* dense;
+  const unsigned* not_dense;  // 0: rows[i] == rows[0] + i for every i
 };
 struct RowMap {
   const uint32_t* rows;
   bool dense;
   uint32_t base;
   __device__ __forceinline__ explicit RowMap(const BuildRows& b)
-      : rows(b.rows), dense(*b.dense != 0), base(dense ? b.rows[0] : 0u) {}
+      : rows(b.rows), dense(*b.not_dense == 0), base(dense ? b.rows[0] : 0u) {}
   __device__ __forceinline__ uint32_t operator()(uint32_t p) const { return dense ? base + p : __ldg(rows + p); }
 };
 
