@@ -887,9 +887,7 @@ int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint6
       void* args[] = {&f};
       CK(cudaLaunchCooperativeKernel((void*)topk_fused_kernel, blocks, kSelThreads, args, smem, s));
       ++g_launches;
-      prof_record(1, s);
-      prof_record(2, s);
-      prof_record(3, s);
+      prof_record(3, s);  // one kernel: select time = events 0 -> 3 (no graph nodes for 1, 2)
       g.topk_pending = true;  // candidate count / fallback resolved lazily
       if (g.prof) {
         g.kt.topk_threshold_ms = g.kt.topk_filter_ms = 0.0;

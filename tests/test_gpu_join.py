@@ -197,6 +197,29 @@ def test_partitioned_probe_hot_key_overflows_slice(b200, monkeypatch, hot):
     assert np.array_equal(res.payload.probe_rows, ep) and np.array_equal(res.payload.build_rows, eb)
 
 
+@pytest.mark.parametrize("rows_kind", ["high", "mixed", "dense_high_base"])
+def test_two_member_groups_with_large_row_ids(b200, rows_kind):
+    """Key groups of two keep both rows in the slot only when the second row
+    fits 30 bits; row ids at and above 2^30 take the side-array path, and a
+    dense column starting near 2^32 keeps positions. Pairs and order must match."""
+    rng = np.random.default_rng(len(rows_kind))
+    nb, np_ = 300_000, 1_000_000
+    bk = rng.integers(0, 400_000, size=nb).astype(np.float64)  # many groups of two
+    if rows_kind == "high":
+        br = rng.choice(np.arange(1 << 30, (1 << 32) - 1, dtype=np.uint64), size=nb, replace=False).astype(np.uint32)
+    elif rows_kind == "mixed":
+        br = rng.permutation(nb).astype(np.uint32)
+        br[rng.random(nb) < 0.5] |= np.uint32(1 << 30)
+    else:
+        br = (np.arange(nb, dtype=np.uint64) + ((1 << 32) - nb - 5)).astype(np.uint32)
+    pk = rng.integers(0, 400_000, size=np_).astype(np.float64)
+    pr = np.arange(np_, dtype=np.uint32)
+    res = b200.probe(KeyVector(bk, br), KeyVector(pk, pr))
+    ep, eb = oracle.join(bk, br, pk, pr)
+    assert res.payload.match_count == len(ep)
+    assert np.array_equal(res.payload.probe_rows, ep) and np.array_equal(res.payload.build_rows, eb)
+
+
 def test_partitioned_join_natural_scale(cuda):
     """A table above the partitioning threshold with default settings (1 GiB
     table, 64 slices, probe side partitioned) against the oracle."""
