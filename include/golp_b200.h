@@ -121,6 +121,9 @@ int golp_set_dense_rows(int on);
  * positions as extract_keys passes them (store.py:178-181): the host-side scan
  * that verifies this is skipped (the end points are still checked). */
 int golp_hint_dense_rows(void);
+/* 0: off; 1: timing events around each kernel group of every call; 2: the same
+ * without the event at a join build's start (join_build_ms stays 0), which
+ * saves one event node per CUDA-graph step when only the probe is timed. */
 int golp_set_profiling(int on);
 int golp_last_kernel_times(golp_kernel_times* out);
 

@@ -139,6 +139,7 @@ struct Ctx {
   char* status_dev = nullptr;
   bool prof = false;
   bool build_timed = false;
+  bool prof_build_start = true;  // golp_set_profiling(2) drops the build-start event
   bool probe_timed = false;
   bool topk_pending = false;  // fused Top-K in flight: candidates/fallback read on demand
   bool topk_timed = false;
@@ -1114,7 +1115,7 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
     CK(g.grp_bits.ensure((cap + 31) / 32 * 4));
     ga.grp_bits = g.grp_bits.as<uint32_t>();
   }
-  prof_record(4, s);
+  if (g.prof_build_start) prof_record(4, s);
   join_init_table_kernel<<<grid_for(cap, 256, 8), 256, 0, s>>>(table, cap, ga.grp_bits, brows, nb,
                                                                 check ? 0 : (rows_dense ? 1 : 2), dflag, dflag_next,
                                                                 ga.counters);
@@ -1530,6 +1531,7 @@ int golp_set_profiling(int on) {
   Ctx& g = cur();
   RET(ensure_init());
   g.prof = on != 0;
+  g.prof_build_start = on != 2;
   g.build_timed = g.probe_timed = g.topk_timed = false;
   return GOLP_OK;
 }
@@ -1656,7 +1658,8 @@ int golp_join_build_device(const double* d_build_keys, const uint32_t* d_build_r
   RET(check_device_ptr(d_build_keys));
   cudaStream_t s = as_stream(stream);
   RET(join_build_impl(d_build_keys, d_build_rows, nb, s));
-  g.build_timed = g.prof;  // resolved lazily by golp_last_kernel_times (no sync here)
+  g.build_timed = g.prof && g.prof_build_start;  // resolved lazily by golp_last_kernel_times (no sync here)
+  if (g.prof && !g.prof_build_start) g.kt.join_build_ms = 0.0;
   return GOLP_OK;
 }
 

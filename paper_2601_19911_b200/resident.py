@@ -127,5 +127,7 @@ def full_sort(keys: torch.Tensor, rows: torch.Tensor, stream=None) -> torch.Tens
     return out
 
 
-def set_profiling(on: bool) -> None:
-    _native.check(_native.load().golp_set_profiling(1 if on else 0))
+def set_profiling(on: bool, build_start: bool = True) -> None:
+    """Library timing events on/off (golp_set_profiling); build_start=False skips
+    the event at a join build's start (probe phase still timed, build not)."""
+    _native.check(_native.load().golp_set_profiling((1 if build_start else 2) if on else 0))
