@@ -1073,6 +1073,16 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
   Ctx& g = cur();
   uint64_t cap = 1024;
   while (cap < 2 * nb && cap < (1ull << 32)) cap <<= 1;
+#ifndef GOLP_SMALL_TABLE_SPREAD
+#define GOLP_SMALL_TABLE_SPREAD 2
+#endif
+  // tables that stay in L2 either way get extra room: fewer CAS collisions in the
+  // build and fewer second lookups in the probe
+  {
+    const uint64_t spread = env_u64("GOLP_SMALL_TABLE_SPREAD", GOLP_SMALL_TABLE_SPREAD);
+    const uint64_t l2cap = env_u64("GOLP_SMALL_TABLE_BYTES", 64ull << 20) / sizeof(Slot);
+    while (spread > 1 && cap * 2 <= l2cap && cap < 2 * spread * nb && cap < (1ull << 32)) cap <<= 1;
+  }
   if (cap < 2 * nb || cap * kInline + nb > (1ull << 32)) {
     set_error("join build side too large for 32-bit slot / row indices");
     return GOLP_ERR_CAPACITY;
