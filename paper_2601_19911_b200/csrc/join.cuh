@@ -967,9 +967,13 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_ker
 #endif
 constexpr int kPartProbeItems = GOLP_PART_PROBE_ITEMS;
 #ifndef GOLP_PART_PROBE_SUB
-#define GOLP_PART_PROBE_SUB 8
+#define GOLP_PART_PROBE_SUB 16
 #endif
 constexpr int kPartProbeSub = GOLP_PART_PROBE_SUB;
+// fixed-capacity slices are whole partition tiles: a lookup chunk must never
+// straddle two of them (PartExtent::end_of)
+static_assert(kPartTile % ((uint64_t)kProbeThreads * kPartProbeItems * kPartProbeSub) == 0,
+              "lookup chunks must divide the partition tile");
 // Deferred second rounds: a key not resolved by its home pair is queued (per
 // warp, in shared memory) instead of holding its whole warp for another round
 // trip; a full queue is resolved by the warp with all 32 lanes busy. res_part
