@@ -10,7 +10,8 @@
 //   table  : cap x 16 B slots {u64 key_bits, u32 off, u32 cnt}, one slot per
 //            DISTINCT build key. Linear probing whose start is rounded down to an
 //            even slot: the probe walks 32-byte, sector-aligned slot pairs, one
-//            256-bit load per pair (LDG.E.256). cap = pow2 >= 2*nb (load <= 0.5).
+//            256-bit load per pair (LDG.E.256). cap = pow2 >= 2*nb (load <= 0.5),
+//            doubled once more while the table stays within 64 MB (L2-resident).
 //   rows   : cap*kInline + nb u32: groups of 2..kInline keep their rows at
 //            h*kInline, bigger groups a CSR range after that, all in build-position
 //            order; groups of one keep their row inline in slot.off.
