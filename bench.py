@@ -345,17 +345,23 @@ def run_b200(args, wl) -> None:
         del op0, full_bk, full_br
         m_dev = torch.zeros(1, dtype=torch.int64, device=dev)
 
-        def step():
-            # build + probe fully enqueued; the match count stays on the device
-            # (read after the step's end event, checked against the capacity)
+        def step_build():
             if world > 1:
                 fbk = torch.cat(sharded._all_gather_ragged(t_bk))
                 fbr = torch.cat(sharded._all_gather_ragged(t_br))
             else:
                 fbk, fbr = t_bk, t_br
             resident.join_build(fbk, fbr)
+
+        def step_probe():
             resident.join_probe_async(t_pk, t_pr, out_p, out_b, m_dev)
             return m_dev
+
+        def step():
+            # build + probe fully enqueued; the match count stays on the device
+            # (read after the step's end event, checked against the capacity)
+            step_build()
+            return step_probe()
 
         local_units = len(bk) + len(pk_s)
     else:
@@ -373,14 +379,14 @@ def run_b200(args, wl) -> None:
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    # Library timing events around the probe phase (a join's build-start event is
-    # left out: every event is a graph node, ~2.7 us per step; the build time is
-    # reported as the step minus the probe phase).
-    resident.set_profiling(True, build_start=wl["kind"] != "join")
     # One CUDA graph per step where the step is a pure enqueue (no host round
-    # trip): the join step (build + async probe) and the fused C1-sized Top-K.
-    # The library's timing events are captured with it, so the per-kernel times
-    # below still come from events on the launch stream of every replayed step.
+    # trip): the fused C1-sized Top-K, and the join step as two graphs (build,
+    # probe) with a CUDA event on the stream between them, so the probe phase is
+    # timed by that event and the step's end event -- no event nodes inside the
+    # graphs (each costs ~2.7 us per step). Other paths time their kernel groups
+    # with the library's events on the launch stream.
+    split = wl["kind"] == "join" and world == 1 and not args.no_graph
+    resident.set_profiling(not split)
     graph, graph_launches = None, 0
     capturable = wl["kind"] == "join" or (local_units <= 2_000_000 and wl["k"] <= 4096)
     if world == 1 and capturable and not args.no_graph:
@@ -392,12 +398,22 @@ def run_b200(args, wl) -> None:
         stream.wait_stream(side)
         torch.cuda.synchronize()
         l0 = _native.launch_count()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            graph_out = step()
+        if split:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step_build()
+            graph_p = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph_p):
+                graph_out = step_probe()
+        else:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                graph_out = step()
         graph_launches = _native.launch_count() - l0
         torch.cuda.synchronize()
         graph.replay()
+        if split:
+            graph_p.replay()
         torch.cuda.synchronize()
     kern_ms, step_ms = [], []
     fused = False
@@ -409,10 +425,14 @@ def run_b200(args, wl) -> None:
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the events)
             e0 = torch.cuda.Event(enable_timing=True)
+            em = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             if graph is not None:
                 graph.replay()
+                if split:
+                    em.record(stream)
+                    graph_p.replay()
                 out = graph_out
             else:
                 out = step()
@@ -422,7 +442,9 @@ def run_b200(args, wl) -> None:
             if wl["kind"] == "join":
                 assert int(out.item()) <= cap, "pair buffers too small for the timed step"
             kt = _native.kernel_times()
-            if wl["kind"] == "join":
+            if split:
+                kern_ms.append(em.elapsed_time(e1))
+            elif wl["kind"] == "join":
                 kern_ms.append(kt["join_probe_ms"])
             elif kt["topk_filter_ms"] > 0:
                 kern_ms.append(kt["topk_filter_ms"])
@@ -560,7 +582,8 @@ def run_b200(args, wl) -> None:
     device.close()
     if rank == 0:
         details = {"global_units_per_step": units, "units_per_rank": local_units,
-                   "launch": "cuda-graph replay per step" if graph is not None else "eager launches"}
+                   "launch": ("cuda-graph replays per step: build graph, stream event, probe graph" if split
+                              else "cuda-graph replay per step" if graph is not None else "eager launches")}
         if matches_total is not None:
             details["matches"] = matches_total
         line = {
