@@ -22,6 +22,11 @@ echo "c2 launches rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:"join_match_kernel|join_emit_kernel|join_insert|join_finalize" \
   -s 7 -c 4 -o gpurun_out/r2_full_join_c2 python tools/join_breakdown.py 1e6 1e7 2e6 3 > gpurun_out/r2_full_join_c2.log 2>&1
 echo "c2 full rc=$?"
+# the same kernels without ncu's cache flush (--cache-control none): the state the bench's
+# step sees (the table was just built and sits in L2); bench.py's roofline.traffic uses these
+ncu --set full --cache-control none --clock-control none --import-source on -k regex:"join_match_kernel|join_emit_kernel" \
+  -s 4 -c 2 -o gpurun_out/r2_full_join_c2_warm python tools/join_breakdown.py 1e6 1e7 2e6 3 > gpurun_out/r2_full_join_c2_warm.log 2>&1
+echo "c2 warm rc=$?"
 # C4: every probe-phase kernel of one whole 1e8 x 2e9 join, time + DRAM bytes
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   -k regex:"part_|join_|scan_" python tools/join_breakdown.py 1e8 2e9 2e8 1 > gpurun_out/r2_launches_join_c4.csv 2>&1
