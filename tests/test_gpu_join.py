@@ -100,6 +100,53 @@ def test_join_resident_api(cuda):
         resident.join_probe(t(pk), t(pr), small, small.clone())
 
 
+@pytest.mark.parametrize("dense", [True, False])
+def test_join_graph_replay_and_profiling_levels(cuda, dense):
+    """The resident build + async probe captured in CUDA graphs (as bench.py
+    replays them) gives the oracle's pairs on every replay, with the density flag
+    alternating between builds; profiling level 2 times the probe, not the build."""
+    import torch
+
+    from paper_2601_19911_b200 import _native, resident
+
+    rng = np.random.default_rng(31 + dense)
+    nb, np_ = 400_000, 2_000_000
+    bk = rng.integers(0, 800_000, size=nb).astype(np.float64)
+    pk = rng.integers(0, 800_000, size=np_).astype(np.float64)
+    br = np.arange(nb, dtype=np.uint32) + 7 if dense else rng.permutation(nb).astype(np.uint32)
+    pr = np.arange(np_, dtype=np.uint32)
+    t = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(cuda)  # noqa: E731
+    tbk, tbr, tpk, tpr = t(bk), t(br), t(pk), t(pr)
+    ep, eb = oracle.join(bk, br, pk, pr)
+    out_p = torch.empty(len(ep) + 16, dtype=torch.int32, device=cuda)
+    out_b = torch.empty_like(out_p)
+    m = torch.zeros(1, dtype=torch.int64, device=cuda)
+    resident.set_profiling(True, build_start=False)
+    try:
+        resident.join_build(tbk, tbr)
+        resident.join_probe_async(tpk, tpr, out_p, out_b, m)
+        torch.cuda.synchronize()
+        kt = _native.kernel_times()
+        assert kt["join_build_ms"] == 0.0 and kt["join_probe_ms"] > 0.0
+    finally:
+        resident.set_profiling(False)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        gb, gp = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gb):
+            resident.join_build(tbk, tbr)
+        with torch.cuda.graph(gp):
+            resident.join_probe_async(tpk, tpr, out_p, out_b, m)
+    for _ in range(3):
+        out_p.fill_(-1)
+        gb.replay()
+        gp.replay()
+        torch.cuda.synchronize()
+        assert int(m.item()) == len(ep)
+        assert np.array_equal(out_p[: len(ep)].cpu().numpy().view(np.uint32), ep)
+        assert np.array_equal(out_b[: len(ep)].cpu().numpy().view(np.uint32), eb)
+
+
 # ---- radix-partitioned join (tables larger than two slices) -------------------
 # GOLP_JOIN_SLICE_BYTES shrinks the slice so small builds take the partitioned
 # path; GOLP_JOIN_PART_PROBE=1 forces the slice-ordered probe as well.
