@@ -795,10 +795,10 @@ __global__ void __launch_bounds__(kPartThreads, GOLP_PART_MINB) part_scatter_ker
 #pragma unroll
     for (int u = 0; u < kPartItems; ++u) {
       const uint32_t i = threadIdx.x + u * kPartThreads;
-      if (i < cnt) {
-        out.keys[o[u]] = s_key[i];
-        if (out.pos) out.pos[o[u]] = (uint32_t)(t0 + s_loc[i]);
-        if (out.idx) out.idx[o[u]] = s_loc[i];
+      if (i < cnt) {  // streaming stores: read once, by a later kernel
+        __stcs(reinterpret_cast<unsigned long long*>(out.keys) + o[u], (unsigned long long)__double_as_longlong(s_key[i]));
+        if (out.pos) __stcs(out.pos + o[u], (uint32_t)(t0 + s_loc[i]));
+        if (out.idx) __stcs(reinterpret_cast<unsigned short*>(out.idx) + o[u], (unsigned short)s_loc[i]);
       }
     }
     __syncthreads();
@@ -982,6 +982,18 @@ static_assert(kPartTile % ((uint64_t)kProbeThreads * kPartProbeItems * kPartProb
 #ifndef GOLP_PART_PROBE_QUEUE
 #define GOLP_PART_PROBE_QUEUE 1
 #endif
+// Lookup results: written once, read once by match_runs much later -- streaming
+// stores, so they do not push the table slice being probed out of L2.
+#ifndef GOLP_RES_STREAM
+#define GOLP_RES_STREAM 1
+#endif
+__device__ __forceinline__ void st_res(uint64_t* p, uint64_t v) {
+#if GOLP_RES_STREAM
+  __stcs(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+#else
+  *p = v;
+#endif
+}
 struct PartProbeQueue {
   uint64_t bits[32];
   uint32_t h[32];
@@ -1001,7 +1013,7 @@ __device__ __forceinline__ void part_queue_drain(const PartProbeQueue& q, unsign
       if (st >= 0) break;
       h = (h + 2) & (uint32_t)mask;
     }
-    res_part[q.i[lane]] = ((uint64_t)cnt << 32) | off;
+    st_res(res_part + q.i[lane], ((uint64_t)cnt << 32) | off);
   }
   __syncwarp();
 }
@@ -1072,7 +1084,7 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_prob
         int st = 1;
         if (valid) {
           st = check_pair(ldg_pair(table + h, pol_table), bits, off, cnt, true);
-          if (st >= 0) res_part[base] = ((uint64_t)cnt << 32) | off;
+          if (st >= 0) st_res(res_part + base, ((uint64_t)cnt << 32) | off);
         }
         unsigned need = __ballot_sync(0xFFFFFFFFu, st < 0);
         while (need) {  // queue the unresolved lanes; resolve the queue whenever it fills
@@ -1123,7 +1135,7 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_prob
 #pragma unroll
       for (int j = 0; j < kPartProbeItems; ++j) {
         const uint64_t i = base + (uint64_t)j * kProbeThreads;
-        if (i < n) res_part[i] = ((uint64_t)cnt[j] << 32) | off[j];
+        if (i < n) st_res(res_part + i, ((uint64_t)cnt[j] << 32) | off[j]);
         kc[j] = kn[j];
       }
 #endif
