@@ -121,7 +121,6 @@ def test_criterion_07_stream_on_b200(b200):
     cfg = GateConfig(profile=calibrate_device_profile(b200, ns=(10_000, 100_000, 1_000_000), k=spec.k, repeats=9),
                      cpu_model=calibrate_host_topk_model(spec.k, ns=(10_000, 20_000, 50_000, 1_000_000)))
     tables = {}
-    run_strategy_comparison(spec, cfg, device=b200, tables=tables)  # settle after calibration (discarded)
     for _ in range(3):
         host, device, gated = run_strategy_comparison(spec, cfg, device=b200, tables=tables)
         h, d, g = (compute_stats(r.all_samples()) for r in (host, device, gated))

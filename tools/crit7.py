@@ -29,7 +29,6 @@ with B200Device() as dev:
         print(json.dumps({"profile": cfg.profile.to_json_dict() if hasattr(cfg.profile, "to_json_dict") else str(cfg.profile),
                           "cpu_model": cfg.cpu_model.to_json_dict()}), flush=True)
     tables = {}
-    run_strategy_comparison(spec, cfg, device=dev, tables=tables)  # settle (discarded)
     for r in range(runs):
         host, device, gated = run_strategy_comparison(spec, cfg, device=dev, tables=tables)
         row = {}
