@@ -21,8 +21,7 @@ import numpy as np
 from .device import (DEFAULT_MODELED_PROFILE, FULL_ROW, KEY_ONLY, OP_PROBE, OP_TOPK, ModeledDevice, TransferLedger,
                      calibrate_profile)
 from .errors import StrategyMismatchError
-from .gate import (DEFAULT_CPU_MODEL, DEVICE, HOST, OP_FULL_SORT, GateConfig, calibrate_cpu_model, estimate_cpu_cost,
-                   execute_gated, execute_path)
+from .gate import DEFAULT_CPU_MODEL, DEVICE, HOST, OP_FULL_SORT, GateConfig, estimate_cpu_cost, execute_gated, execute_path
 from .host import host_full_sort, host_topk, mix64
 from .store import DEFAULT_MEMORY_BUDGET, DEFAULT_PAYLOAD_BYTES, ColumnTable, generate_table, random_key_vector
 
@@ -311,29 +310,14 @@ def _timed_ledger(device, call):
     rest of the critical path is charged to the transfer phases (the ledger's
     wall-clock split puts only the kernel TAIL after the last upload into
     t_kernel, which does not grow with n: chunks are filtered / probed while
-    later chunks upload). The call's fixed cost outside the ledger (the Python
-    wrapper, argument checks, result objects: wall time minus ledger total) is
-    added to t_kernel, where the fit turns it into launch_overhead, so the
-    phases add up to the wall-clock time of the call the gate will make."""
-    t0 = time.perf_counter()
+    later chunks upload). The phases still add up to the measured call time."""
     led = call().ledger
-    over = max(time.perf_counter() - t0 - led.total, 0.0)
     timer = getattr(device, "last_kernel_seconds", None)
     k = timer() if timer is not None else None
     if not k:
-        return TransferLedger.build(led.h2d_bytes, led.d2h_bytes, led.t_h2d, led.t_kernel + over, led.t_d2h, led.t_post)
+        return led
     t_h2d = max(led.total - k - led.t_d2h - led.t_post, 0.0)
-    return TransferLedger.build(led.h2d_bytes, led.d2h_bytes, t_h2d, k + over, led.t_d2h, led.t_post)
-
-
-def calibrate_host_topk_model(k: int, ns: Sequence[int] = (10_000, 100_000, 1_000_000), repeats: int = 15,
-                              seed: int = 0):
-    """CpuCostModel of this machine's host engine for Top-K: the reference's sort-family
-    form (alpha*n*log2(n) + beta) fitted on wall-clock host_topk medians over `ns`
-    (run_scaling_baseline, backend "host"). The gate's default constants model the
-    reference's NumPy host path; this fits the product's own host engine."""
-    rows = run_scaling_baseline(WorkloadSpec(n_grid=tuple(ns), k=k, repeats=repeats, seed=seed), backend="host")
-    return calibrate_cpu_model([(OP_TOPK, r.n, k, r.median_s) for r in rows if r.op == OP_TOPK])
+    return TransferLedger.build(led.h2d_bytes, led.d2h_bytes, t_h2d, k, led.t_d2h, led.t_post)
 
 
 def calibrate_device_profile(device, ns: Sequence[int] = (100_000, 1_000_000, 4_000_000, 16_000_000), k: int = 100,

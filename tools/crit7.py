@@ -10,8 +10,7 @@ from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2601_19911_b200 import B200Device, GateConfig  # noqa: E402
-from paper_2601_19911_b200.harness import (WorkloadSpec, calibrate_device_profile, calibrate_host_topk_model,  # noqa: E402
-                                           compute_stats, run_strategy_comparison)
+from paper_2601_19911_b200.harness import WorkloadSpec, calibrate_device_profile, compute_stats, run_strategy_comparison  # noqa: E402
 
 import gc
 if "--nogc" in sys.argv:
@@ -21,13 +20,8 @@ spec = WorkloadSpec(n_grid=(10_000, 1_000_000), repeats=250, mix=(0.8, 0.2), see
 out = []
 with B200Device() as dev:
     cfg = GateConfig()
-    if "--calibrated" in sys.argv:  # this box: device profile and host-engine Top-K model
-        # the stream's size range; the host fit gets extra small sizes so its
-        # intercept is the small-query cost, not the worker-pool step above 65536 keys
-        cfg = GateConfig(profile=calibrate_device_profile(dev, ns=(10_000, 100_000, 1_000_000), k=spec.k, repeats=9),
-                         cpu_model=calibrate_host_topk_model(spec.k, ns=(10_000, 20_000, 50_000, 1_000_000)))
-        print(json.dumps({"profile": cfg.profile.to_json_dict() if hasattr(cfg.profile, "to_json_dict") else str(cfg.profile),
-                          "cpu_model": cfg.cpu_model.to_json_dict()}), flush=True)
+    if "--calibrated" in sys.argv:
+        cfg = GateConfig(profile=calibrate_device_profile(dev))
     tables = {}
     for r in range(runs):
         host, device, gated = run_strategy_comparison(spec, cfg, device=dev, tables=tables)
@@ -42,6 +36,5 @@ with B200Device() as dev:
         row["pass"] = ok
         out.append(row)
         print(json.dumps({s: {k: round(v, 4) for k, v in row[s].items() if k.endswith("_ms")} for s in
-                          ("host_only", "device_always", "gated")}), "offload", round(gated.offload_rate, 3),
-              "PASS" if ok else "FAIL", flush=True)
+                          ("host_only", "device_always", "gated")}), "PASS" if ok else "FAIL", flush=True)
 print(json.dumps(out))
