@@ -982,6 +982,9 @@ static_assert(kPartTile % ((uint64_t)kProbeThreads * kPartProbeItems * kPartProb
 #ifndef GOLP_PART_PROBE_QUEUE
 #define GOLP_PART_PROBE_QUEUE 1
 #endif
+#ifndef GOLP_PART_QUEUE_EVERY
+#define GOLP_PART_QUEUE_EVERY 8  // > 0: also resolve a partial queue every this many sub-tiles
+#endif
 // Lookup results: written once, read once by match_runs much later -- streaming
 // stores, so they do not push the table slice being probed out of L2.
 #ifndef GOLP_RES_STREAM
@@ -1103,6 +1106,15 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PART_PROBE_MINB) join_prob
             qn = 0;
           }
         }
+#if GOLP_PART_QUEUE_EVERY > 0
+        // resolve the queue every few sub-tiles even when not full: a queued
+        // entry leaves a hole in its sector of res_part, which costs a DRAM
+        // read-modify-write if the sector leaves L2 before the hole is filled
+        if (((u + 1) % GOLP_PART_QUEUE_EVERY) == 0 && qn) {
+          part_queue_drain(q, lane, qn, table, mask, res_part, pol_table);
+          qn = 0;
+        }
+#endif
         kc[0] = kn[0];
       }
 #else
