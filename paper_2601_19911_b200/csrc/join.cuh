@@ -520,20 +520,52 @@ __device__ __forceinline__ uint4 ldg_stream_u4(const uint32_t* p, uint64_t pol) 
 constexpr int kScanThreads = 1024;
 
 // One block: exclusive scan of the partials, offset by *base_in; writes *total_out.
+// Each warp owns a contiguous chunk: a coalesced pass sums it, one block scan of
+// the warp sums gives each chunk's base, a second coalesced pass writes the
+// prefixes (warp-level scans) -- instead of one block-wide scan round (two
+// barriers) per kScanThreads elements.
 __global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(unsigned long long* partial, uint32_t nparts,
                                                                      const unsigned long long* base_in,
                                                                      unsigned long long* total_out) {
   __shared__ unsigned long long s_w[33];
-  unsigned long long carry = base_in ? *base_in : 0ull;  // null: the probe's first pairs
-  for (uint32_t b0 = 0; b0 < nparts; b0 += blockDim.x) {
-    const uint32_t i = b0 + threadIdx.x;
-    const unsigned long long v = i < nparts ? partial[i] : 0ull;
-    unsigned long long tot;
-    const unsigned long long e = block_excl_scan(v, s_w, &tot);
-    if (i < nparts) partial[i] = carry + e;
-    carry += tot;
+  __shared__ unsigned long long s_base[kScanThreads / 32];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  constexpr unsigned kWarps = kScanThreads / 32;
+  const uint32_t per = ((nparts + kWarps - 1) / kWarps + 31) / 32 * 32;
+  const uint32_t b = warp * per, e = b + per < nparts ? b + per : nparts;
+  unsigned long long sum = 0;
+  for (uint32_t i = b + lane; i < e; i += 32) sum += partial[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+  if (lane == 0) s_base[warp] = sum;
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the warp sums
+    const unsigned long long w = lane < kWarps ? s_base[lane] : 0ull;
+    unsigned long long incl = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if ((int)lane >= o) incl += u;
+    }
+    const unsigned long long base = base_in ? *base_in : 0ull;
+    if (lane < kWarps) s_base[lane] = base + incl - w;
+    if (lane == 31) s_w[0] = base + incl;
   }
-  if (threadIdx.x == 0) *total_out = carry;
+  __syncthreads();
+  unsigned long long run = s_base[warp];
+  for (uint32_t i0 = b; i0 < e; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const unsigned long long v = i < e ? partial[i] : 0ull;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if ((int)lane >= o) incl += u;
+    }
+    if (i < e) partial[i] = run + incl - v;
+    run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+  }
+  if (threadIdx.x == 0) *total_out = s_w[0];
 }
 
 // ---- radix partitioning (tables larger than ~L2/2) ----------------------------------
