@@ -1142,7 +1142,10 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
     ikeys = g.part_keys.as<double>();
     ipos = g.part_pos.as<uint32_t>();
   }
-  int gb = grid_for((nb + kBuildItems - 1) / kBuildItems, kBuildThreads, 8);
+#ifndef GOLP_BUILD_PER_SM
+#define GOLP_BUILD_PER_SM 4
+#endif
+  int gb = grid_for((nb + kBuildItems - 1) / kBuildItems, kBuildThreads, GOLP_BUILD_PER_SM);
   TileSched sched{nullptr};
   if (ipos) {  // partitioned order: blocks claim tiles in order (see TileSched)
     const int grid = resident_grid(join_insert_kernel<true>, kBuildThreads, 0);
