@@ -63,6 +63,27 @@ int golp_host_topk(const double* keys, const uint32_t* rows, uint64_t n, uint64_
     const uint64_t lo = t * step, hi = std::min(n, lo + step);
     if (lo >= hi) return;
     std::vector<HItem>& v = cand[t];
+    if (parts == 1 && kk <= 256 && hi - lo > 8 * kk) {
+      // a small input on the calling thread: a heap of the kk best (its top is
+      // the worst of them) instead of an n-sized copy -- most items are
+      // rejected by one compare and the caller's cache keeps its working set
+      v.reserve(kk);
+      uint64_t i = lo;
+      for (; i < hi && v.size() < kk; ++i) {
+        v.push_back(HItem{ord_key(keys[i]), ~rows[i]});
+        std::push_heap(v.begin(), v.end(), better);
+      }
+      for (; i < hi; ++i) {
+        const uint64_t h = ord_key(keys[i]);
+        if (h < v.front().hi) continue;  // cannot beat the worst kept item
+        const HItem it{h, ~rows[i]};
+        if (!better(it, v.front())) continue;
+        std::pop_heap(v.begin(), v.end(), better);
+        v.back() = it;
+        std::push_heap(v.begin(), v.end(), better);
+      }
+      return;
+    }
     v.resize(hi - lo);
     for (uint64_t i = lo; i < hi; ++i) v[i - lo] = HItem{ord_key(keys[i]), ~rows[i]};
     if (v.size() > kk) {
