@@ -75,7 +75,8 @@ def bench_config(args, wl: dict) -> dict:
     if wl["kind"] == "join":
         cfg.update(build_keys=wl["nb"], probe_keys=wl["np"], key_domain=2 * wl["nb"])
     else:
-        cfg.update(keys=wl["n"], k=wl["k"], dist=wl.get("dist", "uniform"))
+        cfg.update(keys=wl["n"], k=wl["k"], dist=wl.get("dist", "uniform"),
+                   row_ids="u32 column" if getattr(args, "row_column", False) else "positions (arange)")
     return cfg
 
 
@@ -368,7 +369,10 @@ def run_b200(args, wl) -> None:
         keys, rows = topk_data(wl)
         lo, hi = sharded.shard_bounds(len(keys), world, rank)
         t_k = torch.from_numpy(keys[lo:hi]).to(dev)
-        t_r = torch.from_numpy(rows[lo:hi].view(np.int32)).to(dev)
+        # the row ids are the positions (extract_keys's arange): by default the step
+        # passes the shard's first row id instead of a row column (no row loads for
+        # threshold ties); --row-column keeps the u32 column in HBM
+        t_r = torch.from_numpy(rows[lo:hi].view(np.int32)).to(dev) if args.row_column else int(lo)
         k = wl["k"]
 
         def step():
@@ -648,6 +652,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true", help="skip the oracle check of the timed output")
     ap.add_argument("--no-graph", action="store_true", help="launch every resident step eagerly")
+    ap.add_argument("--row-column", action="store_true",
+                    help="Top-K: pass the row-id column instead of the positions it holds")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -185,6 +185,13 @@ int golp_host_unregister(const void* ptr);
  * (for cross-GPU merges via golp_topk_merge_device). */
 int golp_topk_device(const double* d_keys, const uint32_t* d_rows, uint64_t n, uint64_t k,
                      uint32_t* d_out_rows, uint64_t* d_out_keys, void* stream);
+/* golp_topk_device whose row ids are the positions themselves, row_base + i:
+ * the key vector extract_keys makes of a table (pkg/src/golp/store.py:178-181,
+ * rows = arange) needs no row column in HBM, and no row loads for threshold
+ * ties (a Zipf head). Same output contract; GOLP_ERR_INVALID when
+ * row_base + n - 1 exceeds 2^32 - 1. */
+int golp_topk_device_positions(const double* d_keys, uint64_t n, uint32_t row_base, uint64_t k,
+                               uint32_t* d_out_rows, uint64_t* d_out_keys, void* stream);
 /* Exact Top-K of n already-encoded candidates (u64 key code, u32 row), e.g. the
  * all-gathered local results of G GPUs. Same output contract as above. */
 int golp_topk_merge_device(const uint64_t* d_key_codes, const uint32_t* d_rows, uint64_t n, uint64_t k,

@@ -85,6 +85,7 @@ SIGNATURES = {
                           C.POINTER(Ledger)]),
     "golp_probe_copy_out": (_int, [_vp, _vp, _u64, C.POINTER(Ledger)]),
     "golp_topk_device": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
+    "golp_topk_device_positions": (_int, [_vp, _u64, _u32, _u64, _vp, _vp, _vp]),
     "golp_topk_merge_device": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
     "golp_join_build_device": (_int, [_vp, _vp, _u64, _vp]),
     "golp_join_probe_device": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, C.POINTER(_u64), _vp]),

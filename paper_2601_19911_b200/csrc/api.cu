@@ -387,10 +387,13 @@ __global__ void fill_dense_rows_kernel(uint32_t* __restrict__ dst, uint32_t base
 // is in flight, and a fill kernel writes it in HBM on the main stream, where
 // every consumer of the column runs (on the copy stream it would hold back the
 // next upload until it finished). Any other column is copied as is. The
-// device therefore sees exactly the caller's row ids either way.
-int upload_rows(uint32_t* dst, const uint32_t* src, uint64_t n, bool* copied = nullptr) {
+// device therefore sees exactly the caller's row ids either way. A consumer that
+// reads rows only through a RowCol (the Top-K kernels) passes `as_rows`: a dense
+// run then becomes positions (RowCol{nullptr, rows[0]}) and nothing is written.
+int upload_rows(uint32_t* dst, const uint32_t* src, uint64_t n, bool* copied = nullptr, RowCol* as_rows = nullptr) {
   Ctx& g = cur();
   if (copied) *copied = false;
+  if (as_rows) *as_rows = RowCol{dst, 0};
   if (!n) return GOLP_OK;
   const double tv = wall_seconds();
   // A caller-declared dense column (golp_hint_dense_rows: the table's own
@@ -400,6 +403,10 @@ int upload_rows(uint32_t* dst, const uint32_t* src, uint64_t n, bool* copied = n
   if (std::getenv("GOLP_TRACE"))
     std::fprintf(stderr, "[golp] rows [%llu] verified in %.3f ms: %s\n", (unsigned long long)n, (wall_seconds() - tv) * 1e3,
                  dense ? "dense" : "copied");
+  if (dense && as_rows) {
+    *as_rows = RowCol{nullptr, src[0]};
+    return GOLP_OK;
+  }
   if (dense) {
     const int grid = (int)std::min<uint64_t>((n + 1023) / 1024, (uint64_t)g.sms * 8);
     fill_dense_rows_kernel<<<grid, 256, 0, g.s_main>>>(dst, src[0], n);
@@ -712,7 +719,7 @@ int ensure_topk_ws(uint64_t kk, uint64_t cap) {
   return GOLP_OK;
 }
 
-int launch_filter(const double* keys, const uint32_t* rows, uint64_t n, uint64_t cap, cudaStream_t s) {
+int launch_filter(const double* keys, RowCol rows, uint64_t n, uint64_t cap, cudaStream_t s) {
   Ctx& g = cur();
   if (n == 0) return GOLP_OK;
   const uint64_t vec = n / 2 + 1;
@@ -820,7 +827,7 @@ SelectArgs<SrcCand> cand_args(uint64_t kk, uint64_t cap, uint32_t* out_rows, uin
 }
 
 // Exact fallback: radix select straight over the device-resident input.
-int topk_direct(const double* keys, const uint32_t* rows, uint64_t n, uint64_t kk, uint32_t* out_rows,
+int topk_direct(const double* keys, RowCol rows, uint64_t n, uint64_t kk, uint32_t* out_rows,
                 uint64_t* out_hi, cudaStream_t s) {
   CK(cudaMemsetAsync(ctl(2), 0, sizeof(SelectCtl), s));
   RET(launch_select(make_args(SrcInput{keys, rows}, n, kk, kModeFull, 2, out_rows, out_hi), s));
@@ -828,7 +835,7 @@ int topk_direct(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k
 }
 
 // Top-K over device-resident columns (sampling on the device).
-int topk_device_impl(const double* keys, const uint32_t* rows, uint64_t n, uint64_t k, uint32_t* out_rows,
+int topk_device_impl(const double* keys, RowCol rows, uint64_t n, uint64_t k, uint32_t* out_rows,
                      uint64_t* out_hi, cudaStream_t s) {
   Ctx& g = cur();
   const uint64_t kk = std::min(k, n);
@@ -1582,7 +1589,17 @@ int golp_topk_device(const double* d_keys, const uint32_t* d_rows, uint64_t n, u
   RET(ensure_init());
   if (n > 0 && (!d_keys || !d_rows || !d_out_rows)) return invalid("null device pointer");
   RET(check_device_ptr(d_keys));
-  return topk_device_impl(d_keys, d_rows, n, k, d_out_rows, d_out_keys, as_stream(stream));
+  return topk_device_impl(d_keys, RowCol{d_rows, 0}, n, k, d_out_rows, d_out_keys, as_stream(stream));
+}
+
+int golp_topk_device_positions(const double* d_keys, uint64_t n, uint32_t row_base, uint64_t k,
+                               uint32_t* d_out_rows, uint64_t* d_out_keys, void* stream) {
+  if (k < 1) return invalid("k must be at least 1");
+  if (n > 0 && (uint64_t)row_base + n - 1 > 0xFFFFFFFFull) return invalid("row ids row_base + i exceed u32");
+  RET(ensure_init());
+  if (n > 0 && (!d_keys || !d_out_rows)) return invalid("null device pointer");
+  RET(check_device_ptr(d_keys));
+  return topk_device_impl(d_keys, RowCol{nullptr, row_base}, n, k, d_out_rows, d_out_keys, as_stream(stream));
 }
 
 int golp_full_sort_device(const double* d_keys, const uint32_t* d_rows, uint64_t n, uint32_t* d_out_rows,
@@ -1755,7 +1772,8 @@ int golp_topk_codes(const double* keys, const uint32_t* rows, uint64_t n, uint64
     const bool trace = std::getenv("GOLP_TRACE") != nullptr;
     RET(stage_h2d(dk, keys, n * 8));
     if (trace) std::fprintf(stderr, "[golp] topk %.3f ms keys queued\n", (wall_seconds() - t0) * 1e3);
-    RET(upload_rows(dr, rows, n));
+    RowCol rc{dr, 0};
+    RET(upload_rows(dr, rows, n, nullptr, &rc));
     if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(n * (size_t)payload_bytes));
     CK(cudaEventRecord(ev_chunk, g.s_h2d));
     if (trace) std::fprintf(stderr, "[golp] topk %.3f ms rows queued\n", (wall_seconds() - t0) * 1e3);
@@ -1767,7 +1785,7 @@ int golp_topk_codes(const double* keys, const uint32_t* rows, uint64_t n, uint64
     CK(cudaStreamWaitEvent(s, ev_chunk, 0));
     uint32_t* d_out = g.out_rows.as<uint32_t>();
     RET(kspan_mark(s));
-    RET(topk_device_impl(dk, dr, n, kk, d_out, d_hi, s));
+    RET(topk_device_impl(dk, rc, n, kk, d_out, d_hi, s));
     RET(kspan_mark(s));
     CK(cudaStreamSynchronize(s));  // the fused path is stream-ordered: charge its time to t_kernel
     const double t2 = wall_seconds();
@@ -1804,7 +1822,7 @@ int golp_topk_codes(const double* keys, const uint32_t* rows, uint64_t n, uint64
     CK(cudaMemcpyAsync(dsr, hr, p.s * 4, cudaMemcpyHostToDevice, s));
     g.moved_h2d += p.s * 12;
     CK(cudaMemsetAsync(ctl(0), 0, sizeof(SelectCtl) * 2, s));
-    RET(launch_select(make_args(SrcInput{ds, dsr}, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), s));
+    RET(launch_select(make_args(SrcInput{ds, RowCol{dsr, 0}}, p.s, p.need_s, kModeThreshold, 0, nullptr, nullptr), s));
   }
   // Stream the columns chunk by chunk; filter each chunk as soon as it lands.
   // The rows of chunk c are verified (or copied) after the keys of chunk c+1
@@ -1825,7 +1843,7 @@ int golp_topk_codes(const double* keys, const uint32_t* rows, uint64_t n, uint64
         CK(cudaStreamWaitEvent(s, ev_chunk, 0));
       }
       RET(kspan_mark(s));
-      RET(launch_filter(dk + c0, dr + c0, cn, p.cap, s));
+      RET(launch_filter(dk + c0, RowCol{dr + c0, 0}, cn, p.cap, s));
       RET(kspan_mark(s));
     }
     return GOLP_OK;
@@ -1846,7 +1864,7 @@ int golp_topk_codes(const double* keys, const uint32_t* rows, uint64_t n, uint64
   uint32_t* d_out = g.out_rows.as<uint32_t>();
   RET(kspan_mark(s));
   if (p.direct) {
-    RET(topk_direct(dk, dr, n, kk, d_out, d_hi, s));
+    RET(topk_direct(dk, RowCol{dr, 0}, n, kk, d_out, d_hi, s));
     CK(cudaStreamSynchronize(s));
   } else {
     RET(ensure_status_words());
@@ -1857,7 +1875,7 @@ int golp_topk_codes(const double* keys, const uint32_t* rows, uint64_t n, uint64
     g.kt.topk_candidates = cands;
     if (bad) {
       g.kt.topk_fallback = 1;
-      RET(topk_direct(dk, dr, n, kk, d_out, d_hi, s));
+      RET(topk_direct(dk, RowCol{dr, 0}, n, kk, d_out, d_hi, s));
       CK(cudaStreamSynchronize(s));
     }
   }

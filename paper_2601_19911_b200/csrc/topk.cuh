@@ -53,11 +53,20 @@ struct SelectCtl {
 
 // ---- item sources -------------------------------------------------------------
 
+// A row-id column: the caller's array, or (rows == nullptr) the positions themselves,
+// base + i -- the row ids extract_keys gives a table's key vector
+// (pkg/src/golp/store.py:178-181), which then need no HBM column and no loads.
+struct RowCol {
+  const uint32_t* rows;
+  uint32_t base;
+  __device__ __forceinline__ uint32_t at(uint64_t i) const { return rows ? __ldg(rows + i) : base + (uint32_t)i; }
+};
+
 struct SrcInput {  // the caller's (keys, rows) columns
   const double* keys;
-  const uint32_t* rows;
+  RowCol rows;
   __device__ __forceinline__ uint64_t hi(uint64_t i) const { return ord_key(__ldg(keys + i)); }
-  __device__ __forceinline__ uint32_t lo(uint64_t i) const { return ~__ldg(rows + i); }
+  __device__ __forceinline__ uint32_t lo(uint64_t i) const { return ~rows.at(i); }
 };
 
 struct SrcCand {  // encoded candidate arrays written by the filter (or a merge)
@@ -79,7 +88,7 @@ struct SrcPairs {  // encoded keys + plain row ids (all-gathered local Top-K res
 // alias. 32-bit arithmetic only (64-bit division costs ~100 instructions).
 struct SrcSample {
   const double* keys;
-  const uint32_t* rows;
+  RowCol rows;
   uint64_t n;
   uint32_t w;  // stratum width, >= 1
   __device__ __forceinline__ uint64_t pos(uint64_t i) const {
@@ -87,7 +96,7 @@ struct SrcSample {
     return p < n ? p : n - 1;
   }
   __device__ __forceinline__ uint64_t hi(uint64_t i) const { return ord_key(__ldg(keys + pos(i))); }
-  __device__ __forceinline__ uint32_t lo(uint64_t i) const { return ~__ldg(rows + pos(i)); }
+  __device__ __forceinline__ uint32_t lo(uint64_t i) const { return ~rows.at(pos(i)); }
 };
 
 template <class Src>
@@ -718,13 +727,13 @@ __global__ void __launch_bounds__(kRankThreads) rank_select_kernel(SelectArgs<Sr
 constexpr int kFilterThreads = 256;
 constexpr int kFilterUnroll = 4;  // 4 x 16 B loads in flight per thread
 
-__device__ __forceinline__ bool filter_keep(double k, double tk, uint32_t tr, const uint32_t* rows, uint64_t pos) {
+__device__ __forceinline__ bool filter_keep(double k, double tk, uint32_t tr, RowCol rows, uint64_t pos) {
   if (k > tk) return true;
-  if (k == tk) return __ldg(rows + pos) <= tr;
+  if (k == tk) return rows.at(pos) <= tr;
   return false;
 }
 
-__device__ __forceinline__ void filter_body(const double* __restrict__ keys, const uint32_t* __restrict__ rows,
+__device__ __forceinline__ void filter_body(const double* __restrict__ keys, RowCol rows,
                                             uint64_t n, double tk, uint32_t tr, unsigned long long* cand_count,
                                             uint64_t* __restrict__ cand_hi, uint32_t* __restrict__ cand_lo,
                                             uint64_t cap) {
@@ -745,7 +754,7 @@ __device__ __forceinline__ void filter_body(const double* __restrict__ keys, con
     const unsigned long long slot = warp_append(cand_count, take);
     if (take && slot < cap) {
       cand_hi[slot] = ord_key(keys[pos]);
-      cand_lo[slot] = ~rows[pos];
+      cand_lo[slot] = ~rows.at(pos);
     }
   }
 
@@ -774,7 +783,7 @@ __device__ __forceinline__ void filter_body(const double* __restrict__ keys, con
       uint32_t rr[2 * kFilterUnroll];
 #pragma unroll
       for (int e = 0; e < 2 * kFilterUnroll; ++e)
-        if ((ties >> e) & 1u) rr[e] = __ldg(rows + head + 2 * (wb + lane + (uint64_t)(e >> 1) * stride) + (e & 1));
+        if ((ties >> e) & 1u) rr[e] = rows.at(head + 2 * (wb + lane + (uint64_t)(e >> 1) * stride) + (e & 1));
 #pragma unroll
       for (int e = 0; e < 2 * kFilterUnroll; ++e)
         if (((ties >> e) & 1u) && rr[e] <= tr) flags |= 1u << e;
@@ -789,7 +798,7 @@ __device__ __forceinline__ void filter_body(const double* __restrict__ keys, con
           if (take && slot < cap) {
             const uint64_t p = head + 2 * (wb + lane + (uint64_t)u * stride) + e;
             cand_hi[slot] = ord_key(e ? v[u].y : v[u].x);
-            cand_lo[slot] = ~__ldg(rows + p);
+            cand_lo[slot] = ~rows.at(p);
           }
         }
       }
@@ -799,7 +808,7 @@ __device__ __forceinline__ void filter_body(const double* __restrict__ keys, con
 
 
 __global__ void __launch_bounds__(kFilterThreads) topk_filter_kernel(
-    const double* __restrict__ keys, const uint32_t* __restrict__ rows, uint64_t n, const SelectCtl* thr,
+    const double* __restrict__ keys, RowCol rows, uint64_t n, const SelectCtl* thr,
     unsigned long long* cand_count, uint64_t* __restrict__ cand_hi, uint32_t* __restrict__ cand_lo,
     uint64_t cap) {
   const double tk = *(const volatile double*)&thr->thr_key;
@@ -817,7 +826,7 @@ __global__ void __launch_bounds__(kFilterThreads) topk_filter_kernel(
 // over the input), so the host never has to wait and decide.
 struct FusedTopkArgs {
   const double* keys;
-  const uint32_t* rows;
+  RowCol rows;
   uint64_t n;
   uint64_t need;  // min(k, n)
   uint32_t s;     // samples (<= kRankMax)

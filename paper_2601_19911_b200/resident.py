@@ -35,22 +35,37 @@ def _check_cols(keys: torch.Tensor, rows: torch.Tensor) -> None:
         raise ValueError("keys and rows must be contiguous CUDA tensors")
 
 
-def topk(keys: torch.Tensor, rows: torch.Tensor, k: int, stream=None, want_codes: bool = False):
+def topk(keys: torch.Tensor, rows, k: int, stream=None, want_codes: bool = False):
     """Top-k of device-resident (key, row) columns -> (rows[min(k,n)], codes|None).
 
+    rows is the row-id tensor, or an int `row_base` when the row ids are the
+    positions row_base + i (extract_keys's arange, store.py:178-181): then no
+    row column is read at all (golp_topk_device_positions).
     codes are the order-preserving u64 key codes (int64 storage) of the winners,
     the input of `merge` for cross-GPU reductions.
     """
     if k < 1:
         raise ValueError("k must be at least 1")
-    _check_cols(keys, rows)
+    positions = isinstance(rows, int)
+    if positions:
+        if keys.dtype != torch.float64 or keys.dim() != 1 or not (keys.is_cuda and keys.is_contiguous()):
+            raise ValueError("keys must be a contiguous 1-D float64 CUDA tensor")
+        if rows < 0 or rows + keys.numel() > (1 << 32):
+            raise ValueError("row ids row_base + i must fit u32")
+    else:
+        _check_cols(keys, rows)
     n = keys.numel()
     kk = min(k, n)
     out = torch.empty(kk, dtype=torch.int32, device=keys.device)
     codes = torch.empty(kk, dtype=torch.int64, device=keys.device) if want_codes else None
     lib = _lib(keys)
-    _native.check(lib.golp_topk_device(keys.data_ptr(), rows.data_ptr(), n, k, out.data_ptr() if kk else 0,
-                                       codes.data_ptr() if (codes is not None and kk) else 0, _stream(stream)))
+    oc = codes.data_ptr() if (codes is not None and kk) else 0
+    if positions:
+        _native.check(lib.golp_topk_device_positions(keys.data_ptr(), n, rows, k, out.data_ptr() if kk else 0, oc,
+                                                     _stream(stream)))
+    else:
+        _native.check(lib.golp_topk_device(keys.data_ptr(), rows.data_ptr(), n, k, out.data_ptr() if kk else 0, oc,
+                                           _stream(stream)))
     return out, codes
 
 

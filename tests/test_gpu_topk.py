@@ -209,3 +209,59 @@ def test_topk_large_k_local_and_merge(cuda, k, parts, domain):
     res = [resident.topk(tk[a:b], tr[a:b], k, want_codes=True) for a, b in zip(bounds[:-1], bounds[1:])]
     merged, _ = resident.merge(torch.cat([r[1] for r in res]), torch.cat([r[0] for r in res]), k)
     assert np.array_equal(merged.cpu().numpy().view(np.uint32), expect)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "small_domain", "zipf_hi", "zipf_lo", "signed_zeros"])
+@pytest.mark.parametrize("n,k,base", [(9_000, 100, 0), (1_000_000, 100, 0), (1_000_000, 9000, 12345),
+                                      (3_000_000, 100_000, 0), (3_000_000, 1000, (1 << 32) - 3_000_000)])
+def test_topk_positions_vs_oracle(cuda, kind, n, k, base):
+    """Row ids given as positions (golp_topk_device_positions): no row column, the
+    same answer as the explicit arange column (extract_keys's row ids)."""
+    import torch
+
+    from paper_2601_19911_b200 import resident
+
+    rng = np.random.default_rng(n + k + len(kind))
+    keys = _gen(kind, n, rng)
+    rows = (np.arange(n, dtype=np.uint64) + base).astype(np.uint32)
+    tk = torch.from_numpy(keys).to(cuda)
+    out, codes = resident.topk(tk, base, k, want_codes=True)
+    col, col_codes = resident.topk(tk, torch.from_numpy(rows.view(np.int32)).to(cuda), k, want_codes=True)
+    torch.cuda.synchronize()
+    expect = oracle.topk(keys, rows, k)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), expect)
+    assert torch.equal(out, col) and torch.equal(codes, col_codes)
+
+
+@pytest.mark.parametrize("env", [{"GOLP_TOPK_CAP": "100"}, {"GOLP_TOPK_RANK_MAX": "64"}, {"GOLP_TOPK_FUSED": "0"}])
+def test_topk_positions_fallbacks(cuda, monkeypatch, env):
+    import torch
+
+    from paper_2601_19911_b200 import resident
+
+    for name, v in env.items():
+        monkeypatch.setenv(name, v)
+    n, k, base = 1_000_000, 500, 77
+    keys = _zipf(n, 5, True)
+    rows = np.arange(base, base + n, dtype=np.uint32)
+    out, _ = resident.topk(torch.from_numpy(keys).to(cuda), base, k)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), oracle.topk(keys, rows, k))
+
+
+def test_topk_positions_sharded_merge_and_bounds(cuda):
+    import torch
+
+    from paper_2601_19911_b200 import resident
+
+    n, k = 4_000_001, 1000
+    keys = _zipf(n, 9, True)
+    tk = torch.from_numpy(keys).to(cuda)
+    h = n // 3
+    parts = [resident.topk(tk[lo:hi], lo, k, want_codes=True) for lo, hi in ((0, h), (h, n))]
+    merged, _ = resident.merge(torch.cat([p[1] for p in parts]), torch.cat([p[0] for p in parts]), k)
+    expect = oracle.topk(keys, np.arange(n, dtype=np.uint32), k)
+    assert np.array_equal(merged.cpu().numpy().view(np.uint32), expect)
+    with pytest.raises(ValueError):
+        resident.topk(tk, (1 << 32) - n + 1, k)  # row ids would pass 2^32 - 1
+    lib = _native.load()
+    assert lib.golp_topk_device_positions(tk.data_ptr(), n, (1 << 32) - n + 1, k, 0, 0, 0) != 0
