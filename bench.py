@@ -73,7 +73,8 @@ def bench_config(args, wl: dict) -> dict:
            "scaling": "strong: one global workload, sharded over the GPUs",
            "l2": "flushed between timed steps (256 MiB write outside the CUDA events)"}
     if wl["kind"] == "join":
-        cfg.update(build_keys=wl["nb"], probe_keys=wl["np"], key_domain=2 * wl["nb"])
+        cfg.update(build_keys=wl["nb"], probe_keys=wl["np"], key_domain=2 * wl["nb"],
+                   probe_row_ids="positions (arange)" if getattr(args, "probe_positions", False) else "u32 column")
     else:
         cfg.update(keys=wl["n"], k=wl["k"], dist=wl.get("dist", "uniform"),
                    row_ids="u32 column" if getattr(args, "row_column", False) else "positions (arange)")
@@ -335,7 +336,10 @@ def run_b200(args, wl) -> None:
         t_bk = torch.from_numpy(bk[blo:bhi]).to(dev)
         t_br = torch.from_numpy(br[blo:bhi].view(np.int32)).to(dev)
         t_pk = torch.from_numpy(pk_s).to(dev)
-        t_pr = torch.from_numpy(pr_s.view(np.int32)).to(dev)
+        # the probe row ids are the positions (extract_keys's arange); by default they
+        # travel as a u32 column (12 B per probe); --probe-positions passes
+        # the shard's first row id instead (golp_join_probe_device_positions, 8 B per probe)
+        t_pr = int(lo) if args.probe_positions else torch.from_numpy(pr_s.view(np.int32)).to(dev)
         # size the pair buffers once (first call), then reuse them every step
         full_bk = torch.cat(sharded._all_gather_ragged(t_bk)) if world > 1 else t_bk
         full_br = torch.cat(sharded._all_gather_ragged(t_br)) if world > 1 else t_br
@@ -494,7 +498,8 @@ def run_b200(args, wl) -> None:
     if wl["kind"] == "join":
         table_bytes = int(kt["join_capacity"]) * 16
         l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-        per_probe = 12 + (32 if table_bytes > l2 else 0)
+        # 8-byte key (+ 4-byte row id when a row column is read; positions are computed)
+        per_probe = (8 if args.probe_positions else 12) + (32 if table_bytes > l2 else 0)
         alg_bytes = per_probe * len(pk_s) + 8 * matches
         kernel = "join_probe (join_match_kernel + join_emit_kernel)"
     else:
@@ -654,6 +659,8 @@ def main() -> None:
     ap.add_argument("--no-graph", action="store_true", help="launch every resident step eagerly")
     ap.add_argument("--row-column", action="store_true",
                     help="Top-K: pass the row-id column instead of the positions it holds")
+    ap.add_argument("--probe-positions", action="store_true",
+                    help="joins: pass the probe side's row ids as positions instead of a u32 column")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

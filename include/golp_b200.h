@@ -212,6 +212,16 @@ int golp_join_probe_device(const double* d_probe_keys, const uint32_t* d_probe_r
 int golp_join_probe_device_async(const double* d_probe_keys, const uint32_t* d_probe_rows, uint64_t np,
                                  uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
                                  uint64_t* d_out_matches, void* stream);
+/* The two probes above for a probe key vector whose row ids are its positions,
+ * row_base + i (extract_keys, pkg/src/golp/store.py:178-181): the match kernels
+ * compute the probe row ids instead of reading a u32 column. GOLP_ERR_INVALID
+ * when row_base + np - 1 exceeds 2^32 - 1. */
+int golp_join_probe_device_positions(const double* d_probe_keys, uint64_t np, uint32_t row_base,
+                                     uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
+                                     uint64_t* out_matches, void* stream);
+int golp_join_probe_device_positions_async(const double* d_probe_keys, uint64_t np, uint32_t row_base,
+                                           uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
+                                           uint64_t* d_out_matches, void* stream);
 
 /* Full sort on the device: host_full_sort (host.py:127-130, np.lexsort((rows,
  * keys))) -- d_out_rows gets the n row ids ordered by key ascending (-0.0 ==

@@ -90,6 +90,8 @@ SIGNATURES = {
     "golp_join_build_device": (_int, [_vp, _vp, _u64, _vp]),
     "golp_join_probe_device": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, C.POINTER(_u64), _vp]),
     "golp_join_probe_device_async": (_int, [_vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
+    "golp_join_probe_device_positions": (_int, [_vp, _u64, _u32, _vp, _vp, _u64, C.POINTER(_u64), _vp]),
+    "golp_join_probe_device_positions_async": (_int, [_vp, _u64, _u32, _vp, _vp, _u64, _vp, _vp]),
     "golp_full_sort": (_int, [_vp, _vp, _u64, _int, _u32, _vp, C.POINTER(Ledger)]),
     "golp_full_sort_device": (_int, [_vp, _vp, _u64, _vp, _vp]),
     "golp_host_alloc": (_vp, [_u64]),

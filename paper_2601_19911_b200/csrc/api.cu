@@ -1190,7 +1190,7 @@ int join_build_impl(const double* bkeys, const uint32_t* brows, uint64_t nb, cud
 // (C4-sized tables) first partition each span and look its keys up slice by
 // slice. Pair offsets continue from *base_in; *total_out = *base_in + pairs of
 // this call.
-int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
+int launch_probe(const double* pkeys, RowCol prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
                  uint64_t cap, const unsigned long long* base_in, unsigned long long* total_out, cudaStream_t s) {
   Ctx& g = cur();
   if (np == 0 || g.jnb == 0) {  // base_in null: no pairs before this probe
@@ -1239,11 +1239,11 @@ int launch_probe(const double* pkeys, const uint32_t* prows, uint64_t np, uint32
         const uint64_t tile0 = (c0 - s0) / kPartTile;  // sub-chunks start on partition tiles
         RET(smem_attr(join_match_runs_kernel, kRunSmem));
         join_match_runs_kernel<<<(unsigned)blocks, kProbeThreads, kRunSmem, s>>>(
-            prows + c0, cn, g.res_part.as<uint64_t>(), g.part_pos.as<uint16_t>(),
+            prows.from(c0), cn, g.res_part.as<uint64_t>(), g.part_pos.as<uint16_t>(),
             g.run_base.as<uint32_t>() + tile0 * g.jparts, g.run_len.as<uint16_t>() + tile0 * g.jparts, g.jparts, sc,
             part);
       } else {
-        join_match_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(pkeys + c0, prows + c0, cn, g.table.as<Slot>(),
+        join_match_kernel<<<(unsigned)blocks, kProbeThreads, 0, s>>>(pkeys + c0, prows.from(c0), cn, g.table.as<Slot>(),
                                                                      g.jmask, sc, nwt, per_warp, part);
       }
       CKL();
@@ -1282,7 +1282,7 @@ int read_u64(const void* dptr, uint64_t* out, cudaStream_t s) {
 // Match count of a finished probe (one sync).
 int read_probe_total(const void* dptr, uint64_t* out, cudaStream_t s) { return read_u64(dptr, out, s); }
 
-int join_probe_impl(const double* pkeys, const uint32_t* prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
+int join_probe_impl(const double* pkeys, RowCol prows, uint64_t np, uint32_t* out_p, uint32_t* out_b,
                     uint64_t cap, uint64_t* out_m, cudaStream_t s) {
   Ctx& g = cur();
   CK(g.totals.ensure(16));
@@ -1693,35 +1693,72 @@ int golp_join_build_device(const double* d_build_keys, const uint32_t* d_build_r
   return GOLP_OK;
 }
 
-int golp_join_probe_device_async(const double* d_probe_keys, const uint32_t* d_probe_rows, uint64_t np,
-                                 uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
-                                 uint64_t* d_out_matches, void* stream) {
+namespace {
+int probe_device_async(const double* d_probe_keys, RowCol prows, uint64_t np, uint32_t* d_out_probe_rows,
+                       uint32_t* d_out_build_rows, uint64_t cap, uint64_t* d_out_matches, void* stream) {
   Ctx& g = cur();
   RET(ensure_init());
   if (!d_out_matches) return invalid("null d_out_matches");
   RET(check_device_ptr(d_probe_keys));
   cudaStream_t s = as_stream(stream);
   prof_record(6, s);
-  RET(launch_probe(d_probe_keys, d_probe_rows, np, d_out_probe_rows, d_out_build_rows, cap, nullptr,
+  RET(launch_probe(d_probe_keys, prows, np, d_out_probe_rows, d_out_build_rows, cap, nullptr,
                    reinterpret_cast<unsigned long long*>(d_out_matches), s));
   prof_record(7, s);
   g.probe_timed = g.prof;  // resolved lazily by golp_last_kernel_times
   return GOLP_OK;
 }
 
-int golp_join_probe_device(const double* d_probe_keys, const uint32_t* d_probe_rows, uint64_t np,
-                           uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
-                           uint64_t* out_matches, void* stream) {
+int probe_device(const double* d_probe_keys, RowCol prows, uint64_t np, uint32_t* d_out_probe_rows,
+                 uint32_t* d_out_build_rows, uint64_t cap, uint64_t* out_matches, void* stream) {
   RET(ensure_init());
   if (!out_matches) return invalid("null out_matches");
   RET(check_device_ptr(d_probe_keys));
   cudaStream_t s = as_stream(stream);
-  RET(join_probe_impl(d_probe_keys, d_probe_rows, np, d_out_probe_rows, d_out_build_rows, cap, out_matches, s));
+  RET(join_probe_impl(d_probe_keys, prows, np, d_out_probe_rows, d_out_build_rows, cap, out_matches, s));
   if (*out_matches > cap) {
     set_error("probe output exceeds the supplied capacity");
     return GOLP_ERR_CAPACITY;
   }
   return GOLP_OK;
+}
+
+int check_positions(uint64_t n, uint32_t row_base) {
+  if (n > 0 && (uint64_t)row_base + n - 1 > 0xFFFFFFFFull) return invalid("row ids row_base + i exceed u32");
+  return GOLP_OK;
+}
+}  // namespace
+
+int golp_join_probe_device_async(const double* d_probe_keys, const uint32_t* d_probe_rows, uint64_t np,
+                                 uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
+                                 uint64_t* d_out_matches, void* stream) {
+  if (np > 0 && !d_probe_rows) return invalid("null device pointer");
+  return probe_device_async(d_probe_keys, RowCol{d_probe_rows, 0}, np, d_out_probe_rows, d_out_build_rows, cap,
+                            d_out_matches, stream);
+}
+
+int golp_join_probe_device(const double* d_probe_keys, const uint32_t* d_probe_rows, uint64_t np,
+                           uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
+                           uint64_t* out_matches, void* stream) {
+  if (np > 0 && !d_probe_rows) return invalid("null device pointer");
+  return probe_device(d_probe_keys, RowCol{d_probe_rows, 0}, np, d_out_probe_rows, d_out_build_rows, cap, out_matches,
+                      stream);
+}
+
+int golp_join_probe_device_positions_async(const double* d_probe_keys, uint64_t np, uint32_t row_base,
+                                           uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
+                                           uint64_t* d_out_matches, void* stream) {
+  RET(check_positions(np, row_base));
+  return probe_device_async(d_probe_keys, RowCol{nullptr, row_base}, np, d_out_probe_rows, d_out_build_rows, cap,
+                            d_out_matches, stream);
+}
+
+int golp_join_probe_device_positions(const double* d_probe_keys, uint64_t np, uint32_t row_base,
+                                     uint32_t* d_out_probe_rows, uint32_t* d_out_build_rows, uint64_t cap,
+                                     uint64_t* out_matches, void* stream) {
+  RET(check_positions(np, row_base));
+  return probe_device(d_probe_keys, RowCol{nullptr, row_base}, np, d_out_probe_rows, d_out_build_rows, cap,
+                      out_matches, stream);
 }
 
 // ---- host buffers (E2E) -----------------------------------------------------------------
@@ -1981,6 +2018,9 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
     cb.push_back(cb.back() + std::min(len, left));
   }
   const uint64_t nchunks = cb.size() - 1;
+  // each chunk's probe row ids: its slice of the device column, or positions when dense
+  std::vector<RowCol> crows(nchunks, RowCol{nullptr, 0});
+  for (uint64_t c = 0; c < nchunks; ++c) crows[c] = RowCol{dpr + cb[c], 0};
   CK(g.totals.ensure((nchunks + 1) * 8));
   CK(cudaMemsetAsync(g.totals.p, 0, (nchunks + 1) * 8, s));
   RET(ensure_chunk_events(nchunks));
@@ -2033,7 +2073,7 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   auto finish_upload = [&](uint64_t c) -> int {
     const uint64_t c0 = cb[c], cn = cb[c + 1] - c0;
     bool copied = false;
-    RET(upload_rows(dpr + c0, probe_rows + c0, cn, &copied));
+    RET(upload_rows(dpr + c0, probe_rows + c0, cn, &copied, &crows[c]));
     if (mode == GOLP_FULL_ROW) RET(stage_dummy_h2d(cn * (size_t)payload_bytes));
     CK(cudaStreamWaitEvent(s, g.h2d_ev[c], 0));
     if (copied || mode == GOLP_FULL_ROW) {
@@ -2045,7 +2085,7 @@ int golp_probe(const double* build_keys, const uint32_t* build_rows, uint64_t nb
   auto probe_chunk = [&](uint64_t c, uint32_t* op, uint32_t* ob, uint64_t cap_) -> int {
     const uint64_t c0 = cb[c], cn = cb[c + 1] - c0;
     RET(kspan_mark(s));
-    RET(launch_probe(dpk + c0, dpr + c0, cn, op, ob, cap_, totals + c, totals + c + 1, s));
+    RET(launch_probe(dpk + c0, crows[c], cn, op, ob, cap_, totals + c, totals + c + 1, s));
     RET(kspan_mark(s));
     publish_u64_kernel<<<1, 1, 0, s>>>(reinterpret_cast<volatile unsigned long long*>(g.mirror_dev + c + 1),
                                        totals + c + 1);

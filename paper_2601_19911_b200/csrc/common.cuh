@@ -86,6 +86,20 @@ __device__ __forceinline__ bool item_gt(uint64_t ah, uint32_t al, uint64_t bh, u
   return ah > bh || (ah == bh && al > bl);
 }
 
+// A row-id column: the caller's array, or (rows == nullptr) the positions themselves,
+// base + i -- the row ids extract_keys gives a table's key vector
+// (pkg/src/golp/store.py:178-181), which then need no HBM column and no loads.
+struct RowCol {
+  const uint32_t* rows;
+  uint32_t base;
+  __device__ __forceinline__ uint32_t at(uint64_t i) const { return rows ? __ldg(rows + i) : base + (uint32_t)i; }
+  // streaming (evict-first) load: a column read once
+  __device__ __forceinline__ uint32_t at_cs(uint64_t i) const { return rows ? __ldcs(rows + i) : base + (uint32_t)i; }
+  __host__ __device__ __forceinline__ RowCol from(uint64_t c) const {
+    return rows ? RowCol{rows + c, 0} : RowCol{nullptr, base + (uint32_t)c};
+  }
+};
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 // Warp-aggregated append: every lane with `take` gets a unique slot in [base, base+popc).

@@ -925,7 +925,7 @@ __device__ __forceinline__ void finish_match_block(unsigned lane, unsigned warp,
 }
 
 __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_kernel(
-    const double* __restrict__ pkeys, const uint32_t* __restrict__ prows, uint64_t np, const Slot* __restrict__ table,
+    const double* __restrict__ pkeys, RowCol prows, uint64_t np, const Slot* __restrict__ table,
     uint64_t mask, MatchScratch sc, uint64_t nwt, uint64_t per_warp, unsigned long long* __restrict__ bpart) {
   __shared__ unsigned long long s_w[kProbeWarps];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -952,7 +952,7 @@ __global__ void __launch_bounds__(kProbeThreads, GOLP_PROBE_MINB) join_match_ker
     // the probe rows go out with the keys (a load after the lookups would add a
     // dependent round trip to every tile with a hit)
 #pragma unroll
-    for (int j = 0; j < kWarpItems; ++j) prow[j] = first + j < np ? __ldcs(prows + first + j) : 0u;
+    for (int j = 0; j < kWarpItems; ++j) prow[j] = first + j < np ? prows.at_cs(first + j) : 0u;
     uint64_t bits[kWarpItems];
     uint32_t h[kWarpItems];
     unsigned pending = 0;
@@ -1200,7 +1200,7 @@ static_assert(kRunWarpTiles * kProbeWarps * kWarpTile == kPartTile, "partition t
 constexpr size_t kRunSmem = (size_t)kPartTile * 8;
 
 __global__ void __launch_bounds__(kProbeThreads) join_match_runs_kernel(
-    const uint32_t* __restrict__ prows, uint64_t np, const uint64_t* __restrict__ res_part,
+    RowCol prows, uint64_t np, const uint64_t* __restrict__ res_part,
     const uint16_t* __restrict__ idx, const uint32_t* __restrict__ run_base, const uint16_t* __restrict__ run_len,
     uint32_t nparts, MatchScratch sc, unsigned long long* __restrict__ bpart) {
   extern __shared__ __align__(16) uint64_t s_res[];  // kPartTile entries
@@ -1251,7 +1251,7 @@ __global__ void __launch_bounds__(kProbeThreads) join_match_runs_kernel(
 #pragma unroll
   for (int j = 0; j < kWarpItems; ++j) {
     const uint64_t i = lo * kWarpTile + lane * kWarpItems + j;
-    nrow[j] = lo < hi && i < np ? __ldcs(prows + i) : 0u;
+    nrow[j] = lo < hi && i < np ? prows.at_cs(i) : 0u;
   }
   for (uint64_t wt = lo; wt < hi; ++wt) {
     const uint64_t first = wt * kWarpTile + lane * kWarpItems;
@@ -1263,7 +1263,7 @@ __global__ void __launch_bounds__(kProbeThreads) join_match_runs_kernel(
       cnt[j] = (uint32_t)(v >> 32);
       prow[j] = nrow[j];
       const uint64_t i = first + kWarpTile + j;
-      nrow[j] = wt + 1 < hi && i < np ? __ldcs(prows + i) : 0u;
+      nrow[j] = wt + 1 < hi && i < np ? prows.at_cs(i) : 0u;
     }
     pairs_total += warp_append_hits(lane, off, cnt, prow, sc, cursor);
   }

@@ -53,15 +53,6 @@ struct SelectCtl {
 
 // ---- item sources -------------------------------------------------------------
 
-// A row-id column: the caller's array, or (rows == nullptr) the positions themselves,
-// base + i -- the row ids extract_keys gives a table's key vector
-// (pkg/src/golp/store.py:178-181), which then need no HBM column and no loads.
-struct RowCol {
-  const uint32_t* rows;
-  uint32_t base;
-  __device__ __forceinline__ uint32_t at(uint64_t i) const { return rows ? __ldg(rows + i) : base + (uint32_t)i; }
-};
-
 struct SrcInput {  // the caller's (keys, rows) columns
   const double* keys;
   RowCol rows;

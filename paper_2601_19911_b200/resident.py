@@ -89,16 +89,39 @@ def join_build(keys: torch.Tensor, rows: torch.Tensor, stream=None) -> None:
                                                         _stream(stream)))
 
 
-def join_probe(keys: torch.Tensor, rows: torch.Tensor, out_probe: torch.Tensor, out_build: torch.Tensor,
+def _check_positions(keys: torch.Tensor, row_base: int) -> None:
+    if keys.dtype != torch.float64 or keys.dim() != 1 or not (keys.is_cuda and keys.is_contiguous()):
+        raise ValueError("keys must be a contiguous 1-D float64 CUDA tensor")
+    if row_base < 0 or row_base + keys.numel() > (1 << 32):
+        raise ValueError("row ids row_base + i must fit u32")
+
+
+def _probe_sync(lib, keys, rows, op, ob, cap, m, stream) -> int:
+    """golp_join_probe_device, or its _positions form when rows is an int row base."""
+    if isinstance(rows, int):
+        return lib.golp_join_probe_device_positions(keys.data_ptr(), keys.numel(), rows, op.data_ptr(),
+                                                    ob.data_ptr(), cap, C.byref(m), _stream(stream))
+    return lib.golp_join_probe_device(keys.data_ptr(), rows.data_ptr(), keys.numel(), op.data_ptr(),
+                                      ob.data_ptr(), cap, C.byref(m), _stream(stream))
+
+
+def _check_probe(keys, rows) -> None:
+    if isinstance(rows, int):
+        _check_positions(keys, rows)
+    else:
+        _check_cols(keys, rows)
+
+
+def join_probe(keys: torch.Tensor, rows, out_probe: torch.Tensor, out_build: torch.Tensor,
                stream=None) -> int:
     """Probe the last built table into caller buffers; returns the match count M.
+    rows is the probe row-id tensor, or an int row base when the row ids are the
+    positions row_base + i (extract_keys): no row column is read.
     Raises CapacityError (pairs truncated) when M exceeds the buffers."""
-    _check_cols(keys, rows)
+    _check_probe(keys, rows)
     cap = min(out_probe.numel(), out_build.numel())
     m = C.c_uint64(0)
-    _native.check(_lib(keys).golp_join_probe_device(keys.data_ptr(), rows.data_ptr(), keys.numel(),
-                                                        out_probe.data_ptr(), out_build.data_ptr(), cap,
-                                                        C.byref(m), _stream(stream)))
+    _native.check(_probe_sync(_lib(keys), keys, rows, out_probe, out_build, cap, m, stream))
     return int(m.value)
 
 
@@ -106,16 +129,25 @@ def join_probe_async(keys: torch.Tensor, rows: torch.Tensor, out_probe: torch.Te
                      matches: torch.Tensor, stream=None) -> None:
     """Enqueue a probe of the last built table without synchronizing; the match
     count lands in `matches` (int64 CUDA tensor of one element). Pairs beyond the
-    buffers' capacity are dropped: compare matches with the capacity afterwards."""
-    _check_cols(keys, rows)
+    buffers' capacity are dropped: compare matches with the capacity afterwards.
+    rows may be an int row base (positions), as in join_probe."""
+    _check_probe(keys, rows)
     cap = min(out_probe.numel(), out_build.numel())
-    _native.check(_lib(keys).golp_join_probe_device_async(keys.data_ptr(), rows.data_ptr(), keys.numel(),
-                                                              out_probe.data_ptr(), out_build.data_ptr(), cap,
-                                                              matches.data_ptr(), _stream(stream)))
+    lib = _lib(keys)
+    if isinstance(rows, int):
+        _native.check(lib.golp_join_probe_device_positions_async(keys.data_ptr(), keys.numel(), rows,
+                                                                 out_probe.data_ptr(), out_build.data_ptr(), cap,
+                                                                 matches.data_ptr(), _stream(stream)))
+    else:
+        _native.check(lib.golp_join_probe_device_async(keys.data_ptr(), rows.data_ptr(), keys.numel(),
+                                                       out_probe.data_ptr(), out_build.data_ptr(), cap,
+                                                       matches.data_ptr(), _stream(stream)))
 
 
 def join(bkeys, brows, pkeys, prows, capacity: int | None = None, stream=None):
-    """Build + probe -> (probe_rows[M], build_rows[M]) int32 tensors."""
+    """Build + probe -> (probe_rows[M], build_rows[M]) int32 tensors (prows may be an
+    int row base: probe row ids = positions)."""
+    _check_probe(pkeys, prows)
     join_build(bkeys, brows, stream)
     cap = capacity if capacity is not None else max(pkeys.numel(), 1024)
     while True:
@@ -123,8 +155,7 @@ def join(bkeys, brows, pkeys, prows, capacity: int | None = None, stream=None):
         ob = torch.empty(cap, dtype=torch.int32, device=pkeys.device)
         m = C.c_uint64(0)
         lib = _lib(pkeys)
-        rc = lib.golp_join_probe_device(pkeys.data_ptr(), prows.data_ptr(), pkeys.numel(), op.data_ptr(),
-                                        ob.data_ptr(), cap, C.byref(m), _stream(stream))
+        rc = _probe_sync(lib, pkeys, prows, op, ob, cap, m, stream)
         if rc == _native.GOLP_ERR_CAPACITY:
             cap = int(m.value)
             continue

@@ -406,3 +406,57 @@ def test_resident_topk_and_sort_misaligned_views(cuda):
     assert np.array_equal(got, oracle.topk(keys[1:], rows[1:], 777))
     srt = resident.full_sort(tk, tr).cpu().numpy().view(np.uint32)
     assert np.array_equal(srt, rows[1:][np.lexsort((rows[1:], keys[1:]))])
+
+
+@pytest.mark.parametrize("part_probe,span", [("0", None), ("1", None), ("1", "12288")])
+@pytest.mark.parametrize("base", [0, 1000, (1 << 32) - 2_000_000])
+def test_join_probe_positions_vs_oracle(cuda, monkeypatch, part_probe, span, base):
+    """Probe row ids given as positions (golp_join_probe_device_positions[_async]):
+    the same pairs, in the same order, as the explicit row column."""
+    import torch
+
+    from paper_2601_19911_b200 import resident
+
+    monkeypatch.setenv("GOLP_JOIN_PART_PROBE", part_probe)
+    if part_probe == "1":
+        monkeypatch.setenv("GOLP_JOIN_SLICE_BYTES", "65536")
+    if span:
+        monkeypatch.setenv("GOLP_JOIN_SPAN", span)
+    rng = np.random.default_rng(base % 1000 + 3)
+    nb, np_ = 300_000, 2_000_000
+    bk = rng.integers(0, 600_000, size=nb).astype(np.float64)
+    pk = rng.integers(0, 600_000, size=np_).astype(np.float64)
+    br = rng.permutation(nb).astype(np.uint32)
+    pr = (np.arange(np_, dtype=np.uint64) + base).astype(np.uint32)
+    t = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(cuda)  # noqa: E731
+    ep, eb = oracle.join(bk, br, pk, pr)
+    op, ob = resident.join(t(bk), t(br), t(pk), base)
+    assert np.array_equal(op.cpu().numpy().view(np.uint32), ep)
+    assert np.array_equal(ob.cpu().numpy().view(np.uint32), eb)
+    out_p = torch.empty(len(ep) + 16, dtype=torch.int32, device=cuda)
+    out_b = torch.empty_like(out_p)
+    m = torch.zeros(1, dtype=torch.int64, device=cuda)
+    resident.join_build(t(bk), t(br))
+    resident.join_probe_async(t(pk), base, out_p, out_b, m)
+    torch.cuda.synchronize()
+    assert int(m.item()) == len(ep)
+    assert np.array_equal(out_p[: len(ep)].cpu().numpy().view(np.uint32), ep)
+    assert np.array_equal(out_b[: len(ep)].cpu().numpy().view(np.uint32), eb)
+
+
+def test_join_probe_positions_bounds(cuda):
+    import torch
+
+    from paper_2601_19911_b200 import _native, resident
+
+    pk = torch.zeros(1000, dtype=torch.float64, device=cuda)
+    resident.join_build(pk[:10].clone(), torch.arange(10, dtype=torch.int32, device=cuda))
+    out = torch.empty(10, dtype=torch.int32, device=cuda)
+    with pytest.raises(ValueError):
+        resident.join_probe(pk, (1 << 32) - 999, out, out.clone())
+    lib = _native.load()
+    m = torch.zeros(1, dtype=torch.int64, device=cuda)
+    assert lib.golp_join_probe_device_positions_async(pk.data_ptr(), 1000, (1 << 32) - 999, out.data_ptr(),
+                                                      out.data_ptr(), 10, m.data_ptr(), 0) != 0
+    assert lib.golp_join_probe_device_async(pk.data_ptr(), 0, 1000, out.data_ptr(), out.data_ptr(), 10,
+                                            m.data_ptr(), 0) != 0  # null row column
