@@ -12,6 +12,9 @@ run --workload topk_c3 --k 10 --steps 10
 run --workload topk_c3 --k 1000 --steps 10
 run --workload topk_c3 --k 100000 --steps 10
 run --workload join_c4 --steps 5
+run --probe-positions
+run --workload join_c4 --steps 5 --probe-positions
+run --workload topk_c3 --k 1000 --dist zipf_hi --steps 10 --row-column
 run --workload topk_c3 --k 1000 --dist zipf_hi --steps 10
 run --workload topk_c3 --k 1000 --dist zipf_lo --steps 10
 # launch list of the default bench command (cold-cache, serialized: shares, not absolutes)
