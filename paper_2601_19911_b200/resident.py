@@ -8,6 +8,7 @@ carried in int32 tensors and reinterpreted as u32 by the library.
 from __future__ import annotations
 
 import ctypes as C
+import numbers
 
 import torch
 
@@ -46,7 +47,8 @@ def topk(keys: torch.Tensor, rows, k: int, stream=None, want_codes: bool = False
     """
     if k < 1:
         raise ValueError("k must be at least 1")
-    positions = isinstance(rows, int)
+    positions = isinstance(rows, numbers.Integral)
+    rows = int(rows) if positions else rows
     if positions:
         if keys.dtype != torch.float64 or keys.dim() != 1 or not (keys.is_cuda and keys.is_contiguous()):
             raise ValueError("keys must be a contiguous 1-D float64 CUDA tensor")
@@ -98,18 +100,20 @@ def _check_positions(keys: torch.Tensor, row_base: int) -> None:
 
 def _probe_sync(lib, keys, rows, op, ob, cap, m, stream) -> int:
     """golp_join_probe_device, or its _positions form when rows is an int row base."""
-    if isinstance(rows, int):
+    if isinstance(rows, numbers.Integral):
         return lib.golp_join_probe_device_positions(keys.data_ptr(), keys.numel(), rows, op.data_ptr(),
                                                     ob.data_ptr(), cap, C.byref(m), _stream(stream))
     return lib.golp_join_probe_device(keys.data_ptr(), rows.data_ptr(), keys.numel(), op.data_ptr(),
                                       ob.data_ptr(), cap, C.byref(m), _stream(stream))
 
 
-def _check_probe(keys, rows) -> None:
-    if isinstance(rows, int):
-        _check_positions(keys, rows)
-    else:
-        _check_cols(keys, rows)
+def _check_probe(keys, rows):
+    """Validates the probe columns -> rows (an int row base, or the row tensor)."""
+    if isinstance(rows, numbers.Integral):
+        _check_positions(keys, int(rows))
+        return int(rows)
+    _check_cols(keys, rows)
+    return rows
 
 
 def join_probe(keys: torch.Tensor, rows, out_probe: torch.Tensor, out_build: torch.Tensor,
@@ -118,7 +122,7 @@ def join_probe(keys: torch.Tensor, rows, out_probe: torch.Tensor, out_build: tor
     rows is the probe row-id tensor, or an int row base when the row ids are the
     positions row_base + i (extract_keys): no row column is read.
     Raises CapacityError (pairs truncated) when M exceeds the buffers."""
-    _check_probe(keys, rows)
+    rows = _check_probe(keys, rows)
     cap = min(out_probe.numel(), out_build.numel())
     m = C.c_uint64(0)
     _native.check(_probe_sync(_lib(keys), keys, rows, out_probe, out_build, cap, m, stream))
@@ -131,10 +135,10 @@ def join_probe_async(keys: torch.Tensor, rows: torch.Tensor, out_probe: torch.Te
     count lands in `matches` (int64 CUDA tensor of one element). Pairs beyond the
     buffers' capacity are dropped: compare matches with the capacity afterwards.
     rows may be an int row base (positions), as in join_probe."""
-    _check_probe(keys, rows)
+    rows = _check_probe(keys, rows)
     cap = min(out_probe.numel(), out_build.numel())
     lib = _lib(keys)
-    if isinstance(rows, int):
+    if isinstance(rows, numbers.Integral):
         _native.check(lib.golp_join_probe_device_positions_async(keys.data_ptr(), keys.numel(), rows,
                                                                  out_probe.data_ptr(), out_build.data_ptr(), cap,
                                                                  matches.data_ptr(), _stream(stream)))
@@ -147,7 +151,7 @@ def join_probe_async(keys: torch.Tensor, rows: torch.Tensor, out_probe: torch.Te
 def join(bkeys, brows, pkeys, prows, capacity: int | None = None, stream=None):
     """Build + probe -> (probe_rows[M], build_rows[M]) int32 tensors (prows may be an
     int row base: probe row ids = positions)."""
-    _check_probe(pkeys, prows)
+    prows = _check_probe(pkeys, prows)
     join_build(bkeys, brows, stream)
     cap = capacity if capacity is not None else max(pkeys.numel(), 1024)
     while True:
