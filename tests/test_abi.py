@@ -111,3 +111,19 @@ def test_host_merge_topk_of_shard_lists(parts, k):
     want = oracle.topk(keys, rows, k)
     assert got.value == len(want)
     np.testing.assert_array_equal(out[: got.value], want)
+
+
+def test_resident_positions_validation_without_gpu():
+    """Row bases that would overflow u32 row ids are refused before any device call."""
+    import torch
+
+    from paper_2601_19911_b200 import resident
+
+    keys = torch.zeros(10, dtype=torch.float64)
+    with pytest.raises(ValueError):
+        resident.topk(keys, 0, 3)  # not a CUDA tensor
+    with pytest.raises(ValueError):
+        resident._check_positions(keys, -1)
+    lib = _native.load()
+    # u32 overflow is checked first: no context or device is touched
+    assert lib.golp_topk_device_positions(None, 10, (1 << 32) - 9, 3, None, None, None) == _native.GOLP_ERR_INVALID
