@@ -111,7 +111,9 @@ def test_criterion_07_stream_on_b200(b200):
     calls as device_always's tail: standalone runs put them 0.3-7% above
     device_always's, inside a long test session up to ~11% (host-side state,
     not a different path, separates them: DESIGN.md §7), so the bound here is
-    25%."""
+    25%. The gate's 1e4 queries take host_only's own path, so their P50s agree up
+    to noise (standalone the gate's is lower; inside the suite the two have
+    measured within 3% either way): 10% bound there. The reference asserts no P50."""
     spec = WorkloadSpec(n_grid=(10_000, 1_000_000), repeats=250, mix=(0.8, 0.2), seed=3)
     assert len(spec.n_grid) * spec.repeats == 500
     tables = {}
@@ -119,7 +121,7 @@ def test_criterion_07_stream_on_b200(b200):
         host, device, gated = run_strategy_comparison(spec, GateConfig(), device=b200, tables=tables)
         h, d, g = (compute_stats(r.all_samples()) for r in (host, device, gated))
         assert 0.1 < gated.offload_rate < 0.3
-        assert g.median < h.median and g.median < d.median
+        assert g.median <= 1.1 * h.median and g.median < d.median
         assert g.p95 <= h.p95 and g.p99 <= h.p99
         assert g.p95 <= 1.25 * d.p95 and g.p99 <= 1.25 * d.p99
 
